@@ -1,0 +1,222 @@
+/*
+ * walkvec_b200 — C ABI of the B200 (sm_100a) RDF2vec hot path.
+ *
+ * Plain C: device pointers, sizes and an opaque cudaStream_t (void*).  No
+ * torch, numpy or C++ types cross this boundary.  Every function returns 0 on
+ * success and a negative status on failure (-1 invalid argument, -2 CUDA
+ * error); wv_last_error() returns the thread-local message.  Buffers are
+ * caller-owned; functions that need scratch take (ws, ws_bytes) sized by the
+ * matching *_workspace_bytes query.  Nothing here allocates device memory.
+ *
+ * Each entry point replaces one function of the reference's Python module
+ * walkvec (/root/reference/pkg/src/walkvec/...); the citation is given per
+ * function.  The reference has no FFI of its own: it is numpy all the way
+ * down, so the binding a maintainer adds is a ctypes shim on the reference
+ * side.
+ */
+#ifndef WALKVEC_B200_H
+#define WALKVEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WV_ABI_VERSION 1
+
+/* generator kinds for walk draws (numpy-compatible streams) */
+#define WV_RNG_PCG64 0  /* numpy default_rng(SeedSequence(...)) — the unmodified reference */
+#define WV_RNG_PHILOX 1 /* numpy Generator(Philox(SeedSequence(...))) */
+
+/* flat-corpus filter modes */
+#define WV_KEEP_ENTITY 0   /* walks.project_corpus(..., "entity")   walks.py:323-341 */
+#define WV_KEEP_PROPERTY 1 /* walks.project_corpus(..., "property") walks.py:323-341 */
+#define WV_KEEP_TOKENS 2   /* w2v._filter_min_count                 w2v.py:146-158  */
+
+/* parameter-store precision for SGNS */
+#define WV_FP32 0
+#define WV_FP64 1
+
+/* SGNS pair source */
+#define WV_PAIRS_NATIVE 0   /* device Feistel permutation + length-class decode + Philox negatives */
+#define WV_PAIRS_EXPLICIT 1 /* caller-supplied pair table, epoch permutation, negatives (replay) */
+
+const char* wv_last_error(void);
+int wv_abi_version(void);
+/* sizeof of the ABI structs (0 WvSgnsDevState, 1 WvSgnsModel, 2 WvSgnsBatch) for binding checks */
+int64_t wv_struct_size(int which);
+int wv_stream_sync(void* stream);
+
+/* numpy SeedSequence(prefix + [index]).generate_state(n64, uint64) on the host.
+ * prefix = little-endian u32 words of the leading entropy integers. */
+int wv_seedseq_generate(const uint32_t* entropy_prefix, int n_prefix, uint64_t index, int n64, uint64_t* out);
+/* element k (0-based) of the numpy u64 stream of PCG64/Philox seeded by that SeedSequence */
+int wv_stream_u64(const uint32_t* entropy_prefix, int n_prefix, uint64_t index, int kind, uint64_t k, uint64_t* out);
+
+/* ---------------------------------------------------------------- graph --
+ * Replaces graph.build_graph (graph.py:74-98): stable CSR by source.
+ * edges: device int64 (E,3) rows (src, pred, dst), all in [0, V).
+ * row_offsets: int64[V+1]; packed_edges: u64[E] = pred << 32 | dst. */
+int64_t wv_csr_workspace_bytes(int64_t E, int64_t V);
+int wv_csr_build(const int64_t* edges, int64_t E, int64_t V, int64_t* row_offsets, uint64_t* packed_edges, void* ws,
+                 int64_t ws_bytes, void* stream);
+/* Graph.col_targets / col_predicates views (graph.py:38-41); either may be NULL */
+int wv_csr_unpack(const uint64_t* packed_edges, int64_t E, int64_t* col_targets, int64_t* col_predicates,
+                  void* stream);
+
+/* ---------------------------------------------------------------- walks --
+ * Replaces walks.random_walks/_walk_shard (walks.py:117-204).  The global work
+ * list is repeat(roots, walk_number); this call computes walkers
+ * [work_begin, work_begin+work_count) of it (multi-GPU shards pass disjoint
+ * ranges; the union is byte-identical to one call over everything).
+ * seed_prefix = u32 words of [rng_seed, 0] (SeedSequence([seed, 0, shard])).
+ * corpus: int32 [work_count, 2*depth+1] padded with -1; lengths: int32[work_count]. */
+int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
+                    const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth, int64_t work_begin,
+                    int64_t work_count, const uint32_t* seed_prefix, int n_prefix, int rng_kind, int32_t* corpus,
+                    int32_t* lengths, void* stream);
+
+/* fixed-width rows -> flat tokens (int32 or int64 by token_bytes) + int64 offsets[n+1]
+ * (the PAD strip + concatenate + cumsum of walks.py:139-141, 181-184) */
+int64_t wv_compact_workspace_bytes(int64_t n_walks);
+int wv_corpus_compact(const int32_t* corpus, const int32_t* lengths, int64_t n_walks, int width, int64_t* offsets,
+                      void* tokens, int token_bytes, void* ws, int64_t ws_bytes, void* stream);
+
+/* duplicate_free (walks.py:186-202) over groups of `group` consecutive walks */
+int64_t wv_dedup_workspace_bytes(int64_t n_walks);
+int wv_duplicate_free(const int32_t* corpus, const int32_t* lengths, int64_t n_walks, int width, int64_t group,
+                      int32_t* out_corpus, int32_t* out_lengths, int64_t* n_kept, void* ws, int64_t ws_bytes,
+                      void* stream);
+
+/* project_corpus (walks.py:323-341) and the min_count token filter (w2v.py:146-158) */
+int64_t wv_filter_workspace_bytes(int64_t n_walks);
+int wv_corpus_filter(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int mode,
+                     const uint8_t* token_mask, int64_t* new_offsets, int32_t* new_tokens, void* ws, int64_t ws_bytes,
+                     void* stream);
+
+/* frequency = bincount(tokens, minlength=V) (w2v.py:147, pipeline.py:217) */
+int wv_token_histogram(const int32_t* tokens, int64_t n_tokens, int64_t vocab_size, int64_t* counts, int zero_first,
+                       void* stream);
+
+/* ----------------------------------------------------------------- BFS ---
+ * Replaces walks.bfs_walks/_bfs_tree (walks.py:207-310). */
+int64_t wv_bfs_workspace_bytes(int64_t vertex_count, int64_t n_roots);
+/* phase 1: walks per root, min(leaves, max_walks_per_root) (<= 0: uncapped, the reference) */
+int wv_bfs_count(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count, const int64_t* roots,
+                 int64_t n_roots, int walk_depth, int64_t max_walks_per_root, int64_t* walk_counts, void* ws,
+                 int64_t ws_bytes, void* stream);
+/* phase 2 (same ws): rows [walk_base[r], walk_base[r]+walk_counts[r]) of the
+ * fixed-width int32 corpus [total, 2*depth+1] (-1 padded) + lengths */
+int wv_bfs_emit(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count, const int64_t* roots,
+                int64_t n_roots, int walk_depth, int64_t max_walks_per_root, const int64_t* walk_base, int32_t* corpus,
+                int32_t* lengths, void* ws, int64_t ws_bytes, void* stream);
+/* PathTable (walks.py:87-103, 284-293) rows of a flat BFS corpus: leaf edge first */
+int wv_path_table(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int64_t* sources, int64_t* targets,
+                  int64_t* walk_ids, void* stream);
+
+/* ---------------------------------------------------------------- SGNS ---
+ * Replaces w2v.train for model="skipgram" (w2v.py:507-576) together with
+ * init_embeddings (:123-131), generate_pairs (:161-191), sample_negatives
+ * (:225-239), sgns_batch_grads (:276-299), _coalesce (:407-416) and RowAdam
+ * (:364-404). */
+typedef struct WvSgnsDevState {
+  int64_t lo;             /* first permuted position of the current batch */
+  int64_t epoch;
+  int64_t batch;          /* batch index within the epoch */
+  int64_t step;           /* optimizer steps so far (dense-mode global step) */
+  double epoch_loss_sum;  /* sum of batch_loss * batch_rows (w2v.py:571) */
+  int64_t epoch_count;
+  int64_t diverged_epoch; /* first non-finite batch (w2v.py:566-567), -1 if none */
+  int64_t diverged_batch;
+  double last_batch_loss;
+  uint32_t block_counter;
+  uint32_t pad;
+  int64_t rows_updated;   /* cumulative unique (row, matrix) updates -- telemetry */
+} WvSgnsDevState;
+
+typedef struct WvSgnsModel {
+  int64_t vocab_size;
+  int vector_size;
+  int precision; /* WV_FP32 / WV_FP64 */
+  int sparse;    /* TrainConfig.use_sparse */
+  int pad;
+  double learning_rate;
+  void* input;   /* [V,d] */
+  void* output;  /* [V,d] */
+  void* m_in;
+  void* v_in;
+  void* m_out;
+  void* v_out;
+  int32_t* steps_in; /* RowAdam.row_steps */
+  int32_t* steps_out;
+  uint8_t* touched_in; /* EmbeddingModel.touched_input */
+  uint8_t* touched_out;
+  uint8_t* modified_in; /* rows whose stored value differs from the init */
+  uint8_t* modified_out;
+  void* dense_g_in; /* [V,d] gradient staging, dense mode only */
+  void* dense_g_out;
+  WvSgnsDevState* state;
+} WvSgnsModel;
+
+typedef struct WvSgnsBatch {
+  int mode; /* WV_PAIRS_NATIVE / WV_PAIRS_EXPLICIT */
+  int negatives;
+  int window;
+  int pad;
+  int64_t batch_rows;
+  int64_t n_pairs;
+  uint64_t seed;
+  /* native */
+  const int32_t* tokens;
+  const int64_t* offsets;
+  const int32_t* walks_by_class;
+  const int64_t* class_len;
+  const int64_t* class_walk_start;
+  const int64_t* class_pair_start;
+  int64_t n_classes;
+  const int32_t* candidates; /* NULL: identity */
+  int64_t n_candidates;
+  /* explicit */
+  const int32_t* pairs;
+  const int64_t* perm;
+  const int32_t* negative_table;
+} WvSgnsBatch;
+
+int wv_sgns_init(int64_t vocab_size, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
+                 void* input_matrix, void* output_matrix, void* stream);
+int wv_sgns_export(int64_t vocab_size, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
+                   int matrix, const void* params, const uint8_t* modified, double* out64, void* stream);
+int64_t wv_pair_index_workspace_bytes(int64_t n_walks);
+int wv_pair_index_build(const int64_t* offsets, int64_t n_walks, int window, int32_t* walks_by_class,
+                        int64_t* class_len, int64_t* class_walk_start, int64_t* class_pair_start, int64_t* n_classes,
+                        int64_t* n_pairs, void* ws, int64_t ws_bytes, void* stream);
+int64_t wv_pairs_workspace_bytes(int64_t n_walks);
+int wv_generate_pairs(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int window, int32_t* pairs,
+                      int64_t* n_pairs_out, void* ws, int64_t ws_bytes, void* stream);
+int64_t wv_candidates_workspace_bytes(int64_t vocab_size);
+int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, uint8_t* keep, int32_t* candidates,
+                  int64_t* n_candidates, void* ws, int64_t ws_bytes, void* stream);
+/* reset the batch cursor to permuted position `start` (a worker's span start) */
+int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, void* stream);
+int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
+                                      int precision);
+int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream);
+#define WV_PHASE_PAIRS 1  /* gather rows, dots, coefficients, grouping keys, batch loss */
+#define WV_PHASE_GROUP 2  /* stable radix sort of contributions by row + segment heads */
+#define WV_PHASE_UPDATE 4 /* one warp per unique row: slot-ordered sum + Adam */
+#define WV_PHASE_ALL 7
+int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int phases,
+                         void* stream);
+
+/* Replica averaging (w2v.py:642-659 _merge_bundles + :719-724 resync), run
+ * after an all-reduce(sum) of the deltas and touch counts across ranks. */
+int wv_replica_delta(const void* params, const void* snapshot, int64_t n, int precision, void* delta, void* stream);
+int wv_replica_apply(void* params, void* snapshot, const void* delta_sum, const float* touch_count, int64_t rows,
+                     int vector_size, int precision, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WALKVEC_B200_H */

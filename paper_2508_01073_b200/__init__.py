@@ -1,0 +1,60 @@
+"""paper_2508_01073_b200: B200-native (sm_100a) RDF2vec hot path.
+
+Drop-in for the reference walkvec package's hot path (random / BFS walk
+extraction, SGNS training, and the graph / pipeline calls around them).
+Compute runs in libwalkvec_b200.so (hand-written CUDA behind a C ABI,
+include/walkvec_b200.h); there is no CPU fallback.
+
+    from paper_2508_01073_b200 import PipelineConfig, fit_transform
+    table = fit_transform(edges, vocab, PipelineConfig(walk_depth=4, walk_number=25))
+
+``install()`` re-points a loaded reference ``walkvec`` package at this
+backend (random_walks, bfs_walks, train, build_graph, extract_walks).
+"""
+
+from ._lib import BackendUnavailable
+from .graph import Graph, build_graph
+from .ingest import PAD, Vocabulary, build_vocabulary, encode_integer_triples
+from .install import install, uninstall
+from .pipeline import EmbeddingTable, PipelineConfig, PipelineError, extract_walks, fit_transform
+from .w2v import (
+    CBOW,
+    SKIPGRAM,
+    EmbeddingModel,
+    TrainConfig,
+    TrainingDiverged,
+    estimate_per_sample_bytes,
+    generate_pairs,
+    init_embeddings,
+    resolve_memory_budget,
+    suggest_batch_size,
+    train,
+)
+from .walks import (
+    BFS,
+    ENTITY,
+    FULL,
+    PROPERTY,
+    RANDOM,
+    SHARD_SIZE,
+    PathTable,
+    Walk,
+    WalkCorpus,
+    bfs_walks,
+    project_corpus,
+    project_entity,
+    project_property,
+    random_walks,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BFS", "CBOW", "ENTITY", "FULL", "PAD", "PROPERTY", "RANDOM", "SHARD_SIZE", "SKIPGRAM",
+    "BackendUnavailable", "EmbeddingModel", "EmbeddingTable", "Graph", "PathTable", "PipelineConfig",
+    "PipelineError", "TrainConfig", "TrainingDiverged", "Vocabulary", "Walk", "WalkCorpus",
+    "bfs_walks", "build_graph", "build_vocabulary", "encode_integer_triples", "estimate_per_sample_bytes",
+    "extract_walks", "fit_transform", "generate_pairs", "init_embeddings", "install", "project_corpus",
+    "project_entity", "project_property", "random_walks", "resolve_memory_budget", "suggest_batch_size",
+    "train", "uninstall",
+]

@@ -1,0 +1,1115 @@
+// SGNS training kernels (skip-gram, negative sampling, per-row Adam).
+//
+// Reference semantics (pkg/src/walkvec/w2v.py):
+//   init_embeddings     :123-131  U(-1/d, 1/d) float64 from SeedSequence([seed,1,0]),
+//                                 input matrix then output matrix
+//   generate_pairs      :161-191  shift-major (s=1..W) blocks (t[i],t[i+s]) then (t[i+s],t[i])
+//   _train_single       :547-576  permutation per epoch, contiguous batches, fresh
+//                                 negatives per batch, non-finite loss -> TrainingDiverged
+//   _sgns_forward /
+//   sgns_batch_grads    :247-299  gradients of the batch-mean BCE loss
+//   _coalesce           :407-416  duplicate rows summed in slot order
+//   RowAdam.update      :384-404  per-row step counts (sparse) / global step (dense)
+//
+// B200 design: one warp per pair gathers the (2+k) rows with 16-byte loads,
+// reduces the (1+k) dots with shuffles and emits the per-pair coefficients
+// plus two [B,d] rows (the centre row u and its gradient).  A stable radix
+// sort groups every contribution by destination row in the reference's slot
+// order; one warp per unique row then sums its contributions and applies
+// Adam in place.  No float atomics: results are deterministic run to run.
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+#include "primitives.cuh"
+#include "../../include/walkvec_b200.h"
+
+namespace wv {
+
+constexpr int kPairThreads = 256;
+constexpr int kPairWarps = kPairThreads / 32;
+constexpr int kOwnerThreads = 256;
+
+// ---------------------------------------------------- precise arithmetic --
+// Explicit rounding so the update mirrors numpy's operation order (no FMA
+// contraction) in the float64 path.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float exp_t(float a) { return expf(a); }
+__device__ __forceinline__ double exp_t(double a) { return exp(a); }
+
+// ------------------------------------------------------ vector row I/O ----
+template <typename T, int EPC>
+struct Chunk {
+  T v[EPC];
+};
+
+template <typename T, int EPC>
+__device__ __forceinline__ Chunk<T, EPC> ld_chunk(const T* p) {
+  Chunk<T, EPC> c;
+  if constexpr (EPC * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      float4 f = __ldg(reinterpret_cast<const float4*>(p));
+      c.v[0] = f.x; c.v[1] = f.y; c.v[2] = f.z; c.v[3] = f.w;
+    } else {
+      double2 f = __ldg(reinterpret_cast<const double2*>(p));
+      c.v[0] = f.x; c.v[1] = f.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) c.v[e] = __ldg(p + e);
+  }
+  return c;
+}
+
+// Coherent load (rows being updated inside the same kernel family).
+template <typename T, int EPC>
+__device__ __forceinline__ Chunk<T, EPC> ld_chunk_rw(const T* p) {
+  Chunk<T, EPC> c;
+  if constexpr (EPC * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      float4 f = *reinterpret_cast<const float4*>(p);
+      c.v[0] = f.x; c.v[1] = f.y; c.v[2] = f.z; c.v[3] = f.w;
+    } else {
+      double2 f = *reinterpret_cast<const double2*>(p);
+      c.v[0] = f.x; c.v[1] = f.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) c.v[e] = p[e];
+  }
+  return c;
+}
+
+template <typename T, int EPC>
+__device__ __forceinline__ void st_chunk(T* p, const Chunk<T, EPC>& c) {
+  if constexpr (EPC * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(p) = make_float4(c.v[0], c.v[1], c.v[2], c.v[3]);
+    } else {
+      *reinterpret_cast<double2*>(p) = make_double2(c.v[0], c.v[1]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) p[e] = c.v[e];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// numpy logaddexp(0, x)
+__device__ __forceinline__ double log1pexp(double x) { return x > 0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
+
+// ------------------------------------------------------------- Feistel ----
+struct Feistel {
+  int half_bits;
+  uint64_t mask;
+  uint64_t keys[4];
+};
+
+__device__ __forceinline__ Feistel make_feistel(uint64_t seed, uint64_t epoch, int64_t n) {
+  Feistel f;
+  int bits = 0;
+  while (bits < 62 && ((uint64_t)(n - 1) >> bits)) ++bits;
+  f.half_bits = (bits + 1) / 2;
+  if (f.half_bits < 1) f.half_bits = 1;
+  f.mask = (1ull << f.half_bits) - 1;
+  uint64_t s = splitmix64(seed * 0x9E3779B97F4A7C15ull + 0x5851F42D4C957F2Dull * (epoch + 1));
+  for (int r = 0; r < 4; ++r) {
+    s = splitmix64(s + r);
+    f.keys[r] = s;
+  }
+  return f;
+}
+
+__device__ __forceinline__ uint64_t feistel_once(const Feistel& f, uint64_t x) {
+  uint64_t L = x >> f.half_bits, R = x & f.mask;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    uint64_t nl = R;
+    R = L ^ (splitmix64(R ^ f.keys[r]) & f.mask);
+    L = nl;
+  }
+  return (L << f.half_bits) | R;
+}
+
+// bijection on [0, n) by cycle walking
+__device__ __forceinline__ uint64_t feistel_perm(const Feistel& f, uint64_t pos, int64_t n) {
+  uint64_t x = feistel_once(f, pos);
+  while (x >= (uint64_t)n) x = feistel_once(f, x);
+  return x;
+}
+
+// pairs of one walk of length L with window W: 2 * sum_{s=1..min(W,L-1)} (L - s)
+__host__ __device__ __forceinline__ int64_t walk_pairs(int64_t L, int W) {
+  int64_t t = 0;
+  for (int s = 1; s <= W && s < L; ++s) t += 2 * (L - s);
+  return t;
+}
+
+// local pair q of a length-L walk -> (centre pos, context pos), reference order:
+// for s: block A (i, i+s) for i in [0, L-s), then block B (i+s, i).
+__device__ __forceinline__ void walk_pair_pos(int64_t L, int W, int64_t q, int64_t& cpos, int64_t& xpos) {
+  for (int s = 1; s <= W && s < L; ++s) {
+    const int64_t blk = L - s;
+    if (q < blk) {
+      cpos = q;
+      xpos = q + s;
+      return;
+    }
+    q -= blk;
+    if (q < blk) {
+      cpos = q + s;
+      xpos = q;
+      return;
+    }
+    q -= blk;
+  }
+  cpos = xpos = 0;
+}
+
+// ------------------------------------------------------------ the batch ---
+struct PairArgs {
+  int mode;  // WV_PAIRS_NATIVE or WV_PAIRS_EXPLICIT
+  int64_t V;
+  int d;
+  int k;
+  int window;
+  int64_t B;       // rows in this batch
+  int64_t N;       // pairs per epoch
+  uint64_t seed;
+  // native corpus index
+  const int32_t* tokens;
+  const int64_t* offsets;
+  const int64_t* class_len;
+  const int64_t* class_pair_start;  // n_classes + 1
+  const int64_t* class_walk_start;
+  int n_classes;
+  const int32_t* walks_by_class;
+  const int32_t* candidates;  // null => identity over [0, n_candidates)
+  int64_t n_candidates;
+  // explicit replay
+  const int32_t* pairs;  // [N,2]
+  const int64_t* perm;   // [N] epoch permutation
+  const int32_t* negatives;  // [N,k] per permuted position
+  // outputs
+  void* U;
+  void* G;
+  void* coef;
+  uint32_t* keys;
+  uint32_t* vals;
+  double* partials;
+  WvSgnsDevState* state;
+  uint32_t* seg_count;
+};
+
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(kPairThreads) sgns_pair_kernel(PairArgs A, const T* __restrict__ in,
+                                                                   const T* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = A.d, k = A.k;
+  const int C = d / EPC;
+  const int64_t B = A.B;
+  const int64_t lo = A.state->lo;
+  const uint64_t epoch = (uint64_t)A.state->epoch;
+  T* U = (T*)A.U;
+  T* G = (T*)A.G;
+  T* coef = (T*)A.coef;
+  const T invB = (T)1 / (T)B;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.seg_count = 0;
+
+  Feistel fs;
+  if (A.mode == WV_PAIRS_NATIVE) fs = make_feistel(A.seed, epoch, A.N);
+
+  double loss_acc = 0.0;
+  for (int64_t b = blockIdx.x * (int64_t)kPairWarps + warp; b < B; b += (int64_t)gridDim.x * kPairWarps) {
+    const int64_t pos = lo + b;
+    int32_t center, context;
+    if (A.mode == WV_PAIRS_NATIVE) {
+      const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, A.N);
+      int lo_c = 0, hi_c = A.n_classes;  // last class with start <= q
+      while (hi_c - lo_c > 1) {
+        int mid = (lo_c + hi_c) >> 1;
+        if (A.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
+      }
+      const int64_t L = A.class_len[lo_c];
+      const int64_t np = walk_pairs(L, A.window);
+      const int64_t r = q - A.class_pair_start[lo_c];
+      const int64_t wslot = r / np;
+      const int64_t local = r - wslot * np;
+      const int64_t walk = A.walks_by_class[A.class_walk_start[lo_c] + wslot];
+      int64_t cpos, xpos;
+      walk_pair_pos(L, A.window, local, cpos, xpos);
+      const int64_t base = A.offsets[walk];
+      center = A.tokens[base + cpos];
+      context = A.tokens[base + xpos];
+    } else {
+      const int64_t pi = A.perm[pos];
+      center = A.pairs[2 * pi];
+      context = A.pairs[2 * pi + 1];
+    }
+    // native negatives: Philox4x32 counter (epoch, position, call)
+    uint32_t rnd[4];
+    int rnd_left = 0;
+    int call = 0;
+
+    const T* urow = in + (int64_t)center * d;
+    const T* vrow = out + (int64_t)context * d;
+    Chunk<T, EPC> u[MAXC], g[MAXC], acc[MAXC];
+    T dot = 0;
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int c = lane + 32 * q;
+      if (c < C) {
+        u[q] = ld_chunk<T, EPC>(urow + c * EPC);
+        Chunk<T, EPC> v = ld_chunk<T, EPC>(vrow + c * EPC);
+        g[q] = v;  // keep v until gpos is known
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          dot += u[q].v[e] * v.v[e];
+          acc[q].v[e] = 0;
+        }
+      }
+    }
+    const T pos_logit = warp_sum(dot);
+    double l = log1pexp(-(double)pos_logit);
+    const T gpos = (T(1) / (T(1) + exp_t(-pos_logit)) - T(1)) * invB;
+    if (lane == 0) {
+      coef[b * (k + 1)] = gpos;
+      A.keys[b] = (uint32_t)center;
+      A.vals[b] = (uint32_t)b;
+      A.keys[B + b] = (uint32_t)(context + A.V);
+      A.vals[B + b] = (uint32_t)(B + b);
+    }
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int c = lane + 32 * q;
+      if (c < C) {
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) g[q].v[e] = mul_rn(gpos, g[q].v[e]);
+      }
+    }
+    for (int j = 0; j < k; ++j) {
+      int32_t neg;
+      if (A.mode == WV_PAIRS_NATIVE) {
+        if (rnd_left == 0) {
+          rnd[0] = (uint32_t)pos;
+          rnd[1] = (uint32_t)((uint64_t)pos >> 32);
+          rnd[2] = (uint32_t)epoch;
+          rnd[3] = (uint32_t)call++;
+          philox4x32_10(rnd, (uint32_t)A.seed ^ 0xA5A5F00Du, (uint32_t)(A.seed >> 32) ^ 0x3C6EF372u);
+          rnd_left = 2;
+        }
+        const uint64_t r64 = ((uint64_t)rnd[2 * (2 - rnd_left) + 1] << 32) | rnd[2 * (2 - rnd_left)];
+        --rnd_left;
+        const int64_t idx = (int64_t)mulhi64(r64, (uint64_t)A.n_candidates);
+        neg = A.candidates ? A.candidates[idx] : (int32_t)idx;
+      } else {
+        neg = A.negatives[pos * k + j];
+      }
+      const T* nrow = out + (int64_t)neg * d;
+      Chunk<T, EPC> nv[MAXC];
+      T nd = 0;
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int c = lane + 32 * q;
+        if (c < C) {
+          nv[q] = ld_chunk<T, EPC>(nrow + c * EPC);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) nd += u[q].v[e] * nv[q].v[e];
+        }
+      }
+      const T neg_logit = warp_sum(nd);
+      l += log1pexp((double)neg_logit);
+      const T gneg = (T(1) / (T(1) + exp_t(-neg_logit))) * invB;
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int c = lane + 32 * q;
+        if (c < C) {
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) acc[q].v[e] = add_rn(acc[q].v[e], mul_rn(gneg, nv[q].v[e]));
+        }
+      }
+      if (lane == 0) {
+        coef[b * (k + 1) + 1 + j] = gneg;
+        const int64_t slot = B + b * k + j;
+        A.keys[B + slot] = (uint32_t)(neg + A.V);
+        A.vals[B + slot] = (uint32_t)(B + slot);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int c = lane + 32 * q;
+      if (c < C) {
+        Chunk<T, EPC> gg;
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) gg.v[e] = add_rn(g[q].v[e], acc[q].v[e]);
+        st_chunk<T, EPC>(G + b * d + c * EPC, gg);
+        st_chunk<T, EPC>(U + b * d + c * EPC, u[q]);
+      }
+    }
+    loss_acc += l;  // identical on all lanes
+  }
+
+  // deterministic batch-loss reduction: per-block partial, last block sums
+  __shared__ double wl[kPairWarps];
+  __shared__ bool is_last;
+  if (lane == 0) wl[warp] = loss_acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < kPairWarps; ++w) s += wl[w];
+    A.partials[blockIdx.x] = s;
+    __threadfence();
+    unsigned done = atomicAdd(&A.state->block_counter, 1u);
+    is_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0;
+    for (unsigned i = 0; i < gridDim.x; ++i) s += ((volatile double*)A.partials)[i];
+    WvSgnsDevState* st = A.state;
+    st->block_counter = 0;
+    const double batch_loss = s / (double)B;
+    if (!isfinite(batch_loss) && st->diverged_batch < 0) {
+      st->diverged_batch = st->batch;
+      st->diverged_epoch = st->epoch;
+    }
+    st->epoch_loss_sum += batch_loss * (double)B;
+    st->epoch_count += B;
+    st->last_batch_loss = batch_loss;
+  }
+}
+
+// Segment heads of the sorted contribution keys; also advances the batch cursor.
+__global__ void seg_heads(const uint32_t* __restrict__ keys, int64_t n, int64_t* __restrict__ seg_start,
+                          uint32_t* __restrict__ seg_count, WvSgnsDevState* state, int64_t B) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool head = i < n && (i == 0 || keys[i] != keys[i - 1]);
+    uint32_t m = __ballot_sync(0xffffffffu, head);
+    uint32_t wbase = 0;
+    if (lane == 0 && m) wbase = atomicAdd(seg_count, (uint32_t)__popc(m));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (head) seg_start[wbase + __popc(m & ((1u << lane) - 1u))] = i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state->lo += B;
+    state->batch += 1;
+    state->step += 1;
+  }
+}
+
+struct OwnerArgs {
+  int64_t V;
+  int d;
+  int k;
+  int64_t B;
+  int64_t n_items;
+  const uint32_t* keys;
+  const uint32_t* vals;
+  const int64_t* seg_start;
+  const uint32_t* seg_count;
+  const void* U;
+  const void* G;
+  const void* coef;
+  void* in;
+  void* out;
+  void* m_in;
+  void* v_in;
+  void* m_out;
+  void* v_out;
+  int32_t* steps_in;
+  int32_t* steps_out;
+  uint8_t* touched_in;
+  uint8_t* touched_out;
+  uint8_t* modified_in;
+  uint8_t* modified_out;
+  double lr;
+  int sparse;          // 1: RowAdam sparse mode; 0: write dense gradient rows
+  void* dense_g_in;    // dense mode gradient staging [V,d]
+  void* dense_g_out;
+  WvSgnsDevState* state;
+};
+
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(kOwnerThreads) sgns_owner_kernel(OwnerArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int warps_total = gridDim.x * (kOwnerThreads / 32);
+  const int gw = blockIdx.x * (kOwnerThreads / 32) + (threadIdx.x >> 5);
+  const int d = A.d, k = A.k;
+  const int C = d / EPC;
+  const int64_t B = A.B;
+  const uint32_t nseg = *A.seg_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) A.state->rows_updated += nseg;
+  const T* U = (const T*)A.U;
+  const T* G = (const T*)A.G;
+  const T* coef = (const T*)A.coef;
+  const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
+  const T lr = (T)A.lr;
+  for (uint32_t sg = gw; sg < nseg; sg += warps_total) {
+    const int64_t start = A.seg_start[sg];
+    const uint32_t key = A.keys[start];
+    const bool side_out = key >= (uint32_t)A.V;
+    const int64_t row = side_out ? (int64_t)key - A.V : (int64_t)key;
+    Chunk<T, EPC> g[MAXC];
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) g[q].v[e] = 0;
+    for (int64_t i = start; i < A.n_items && A.keys[i] == key; ++i) {
+      const uint32_t v = A.vals[i];
+      const T* src;
+      T c;
+      if (!side_out) {
+        src = G + (int64_t)v * d;
+        c = 1;
+      } else {
+        const int64_t s = (int64_t)v - B;
+        int64_t p, j;
+        if (s < B) {
+          p = s;
+          j = 0;
+        } else {
+          p = (s - B) / k;
+          j = 1 + (s - B) - p * k;
+        }
+        src = U + p * d;
+        c = coef[p * (k + 1) + j];
+      }
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int cc = lane + 32 * q;
+        if (cc < C) {
+          Chunk<T, EPC> x = ld_chunk<T, EPC>(src + cc * EPC);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) g[q].v[e] = add_rn(g[q].v[e], side_out ? mul_rn(c, x.v[e]) : x.v[e]);
+        }
+      }
+    }
+    T* P = (T*)(side_out ? A.out : A.in);
+    if (!A.sparse) {
+      T* D = (T*)(side_out ? A.dense_g_out : A.dense_g_in);
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int cc = lane + 32 * q;
+        if (cc < C) st_chunk<T, EPC>(D + row * d + cc * EPC, g[q]);
+      }
+      if (lane == 0) (side_out ? A.touched_out : A.touched_in)[row] = 1;
+      continue;
+    }
+    T* M = (T*)(side_out ? A.m_out : A.m_in);
+    T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    int32_t* steps = side_out ? A.steps_out : A.steps_in;
+    int t = 0;
+    if (lane == 0) {
+      t = steps[row] + 1;
+      steps[row] = t;
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const T bc1 = (T)(1.0 - pow(0.9, (double)t));
+    const T bc2 = (T)(1.0 - pow(0.999, (double)t));
+    bool changed = false;
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int cc = lane + 32 * q;
+      if (cc < C) {
+        const int64_t o = row * d + cc * EPC;
+        Chunk<T, EPC> p = ld_chunk_rw<T, EPC>(P + o);
+        Chunk<T, EPC> m = ld_chunk_rw<T, EPC>(M + o);
+        Chunk<T, EPC> vv = ld_chunk_rw<T, EPC>(Vv + o);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const T gr = g[q].v[e];
+          m.v[e] = add_rn(mul_rn(b1, m.v[e]), mul_rn(omb1, gr));
+          vv.v[e] = add_rn(mul_rn(b2, vv.v[e]), mul_rn(mul_rn(omb2, gr), gr));
+          const T mh = div_rn(m.v[e], bc1);
+          const T vh = div_rn(vv.v[e], bc2);
+          const T upd = div_rn(mul_rn(lr, mh), add_rn(sqrt_rn(vh), eps));
+          const T np_ = sub_rn(p.v[e], upd);
+          changed |= (np_ != p.v[e]) || (np_ != np_);
+          p.v[e] = np_;
+        }
+        st_chunk<T, EPC>(P + o, p);
+        st_chunk<T, EPC>(M + o, m);
+        st_chunk<T, EPC>(Vv + o, vv);
+      }
+    }
+    changed = __any_sync(0xffffffffu, changed);
+    if (lane == 0) {
+      (side_out ? A.touched_out : A.touched_in)[row] = 1;
+      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+    }
+  }
+}
+
+// Dense RowAdam (use_sparse=False, w2v.py:396-404): every row decays each
+// batch with the global step; the staged gradient is consumed and zeroed.
+template <typename T>
+__global__ void dense_adam(T* __restrict__ P, T* __restrict__ M, T* __restrict__ Vv, T* __restrict__ Gd,
+                           int64_t n, int d, const WvSgnsDevState* state, double lr, uint8_t* __restrict__ modified) {
+  const int64_t t = state->step;  // already advanced for this batch
+  const T bc1 = (T)(1.0 - pow(0.9, (double)t));
+  const T bc2 = (T)(1.0 - pow(0.999, (double)t));
+  const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8, lrT = (T)lr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T gr = Gd[i];
+    Gd[i] = 0;
+    T m = add_rn(mul_rn(b1, M[i]), mul_rn(omb1, gr));
+    T v = add_rn(mul_rn(b2, Vv[i]), mul_rn(mul_rn(omb2, gr), gr));
+    M[i] = m;
+    Vv[i] = v;
+    const T upd = div_rn(mul_rn(lrT, div_rn(m, bc1)), add_rn(sqrt_rn(div_rn(v, bc2)), eps));
+    const T p = P[i];
+    const T np_ = sub_rn(p, upd);
+    P[i] = np_;
+    if (np_ != p || np_ != np_) modified[i / d] = 1;
+  }
+}
+
+// ------------------------------------------------------------ init/export -
+// Element k of the PCG64 stream SeedSequence([seed,1,0]) -> uniform(-1/d, 1/d).
+// Thread per row: one jump, then d sequential steps.
+__constant__ PcgJump c_pow2_sg[64];
+
+__device__ __forceinline__ PcgJump jump_sg(uint64_t n) {
+  PcgJump r{u128{1, 0}, u128{0, 0}};
+  for (int b = 0; n; ++b, n >>= 1)
+    if (n & 1) r = jump_compose(r, c_pow2_sg[b]);
+  return r;
+}
+
+struct InitStream {
+  u128 state, inc;
+};
+
+template <typename T>
+__global__ void init_rows(InitStream g0, int64_t V, int d, int64_t row_begin, int64_t row_count, int matrix,
+                          T* __restrict__ dst, const uint8_t* __restrict__ only_if_clear, double* __restrict__ dst64) {
+  const double bound = 1.0 / (double)d;
+  const double lower = -bound, range = bound - (-bound);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < row_count; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = row_begin + r;
+    if (only_if_clear && only_if_clear[row]) continue;
+    const uint64_t k0 = (uint64_t)matrix * (uint64_t)V * d + (uint64_t)row * d;
+    PcgJump j = jump_sg(k0 + 1);
+    u128 x = add128(mul128(j.A, g0.state), mul128(g0.inc, j.S));
+    const u128 a1{PCG_MULT_LO, PCG_MULT_HI};
+    for (int c = 0; c < d; ++c) {
+      const double u = u64_to_double(pcg_output(x));
+      const double val = __dadd_rn(lower, __dmul_rn(range, u));
+      if (dst64) dst64[row * d + c] = val;
+      else dst[row * d + c] = (T)val;
+      x = add128(mul128(a1, x), g0.inc);
+    }
+  }
+}
+
+template <typename T>
+__global__ void export_rows(const T* __restrict__ src, int64_t n, double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (double)src[i];
+}
+
+// ------------------------------------------------------- pair indexing ---
+__global__ void walk_len_keys(const int64_t* __restrict__ offsets, int64_t n_walks, uint32_t* __restrict__ keys,
+                              uint32_t* __restrict__ vals) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t L = offsets[w + 1] - offsets[w];
+    keys[w] = (uint32_t)(L > 0xffffffffLL ? 0xffffffffLL : L);
+    vals[w] = (uint32_t)w;
+  }
+}
+
+__global__ void class_heads(const uint32_t* __restrict__ keys, int64_t n, uint8_t* __restrict__ head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void class_fill(const uint32_t* __restrict__ keys, int64_t n, const uint8_t* __restrict__ head,
+                           const int64_t* __restrict__ cls, int64_t* __restrict__ class_len,
+                           int64_t* __restrict__ class_walk_start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (head[i]) {
+      class_len[cls[i]] = keys[i];
+      class_walk_start[cls[i]] = i;
+    }
+}
+
+__global__ void class_pairs(const int64_t* __restrict__ class_len, const int64_t* __restrict__ class_walk_start,
+                            const int64_t* __restrict__ n_classes_p, int64_t n_walks, int window,
+                            int64_t* __restrict__ class_pairs_out) {
+  const int64_t nc = *n_classes_p;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t end = (c + 1 < nc) ? class_walk_start[c + 1] : n_walks;
+    class_pairs_out[c] = (end - class_walk_start[c]) * walk_pairs(class_len[c], window);
+  }
+}
+
+// Reference-order pair materialisation (generate_pairs, w2v.py:177-190):
+// for s in 1..W: block A = (t[i], t[i+s]) over valid flat i, block B swapped.
+// shift_start[s-1] = first output row of shift s; walk_prefix[s-1][w] =
+// valid positions of shift s in walks before w.
+__global__ void pairs_per_walk(const int64_t* __restrict__ offsets, int64_t n_walks, int s,
+                               int64_t* __restrict__ cnt) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t L = offsets[w + 1] - offsets[w];
+    cnt[w] = L > s ? L - s : 0;
+  }
+}
+
+__global__ void pairs_emit(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets, int64_t n_walks,
+                           int s, const int64_t* __restrict__ prefix, const int64_t* __restrict__ n_s_p,
+                           int64_t block_base, int32_t* __restrict__ pairs) {
+  const int64_t n_s = *n_s_p;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = offsets[w];
+    const int64_t L = offsets[w + 1] - o;
+    int64_t r = block_base + prefix[w];
+    for (int64_t i = 0; i + s < L; ++i, ++r) {
+      const int32_t a = tokens[o + i], b = tokens[o + i + s];
+      pairs[2 * r] = a;
+      pairs[2 * r + 1] = b;
+      pairs[2 * (r + n_s)] = b;
+      pairs[2 * (r + n_s) + 1] = a;
+    }
+  }
+}
+
+__global__ void state_reset_epoch(WvSgnsDevState* st, int64_t epoch, int64_t start) {
+  st->lo = start;
+  st->epoch = epoch;
+  st->batch = 0;
+  st->epoch_loss_sum = 0.0;
+  st->epoch_count = 0;
+  st->block_counter = 0;
+}
+
+__global__ void flags_to_candidates(const int64_t* __restrict__ freq, int64_t V, int64_t min_count,
+                                    uint8_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    keep[i] = freq[i] >= min_count ? 1 : 0;
+}
+
+__global__ void scatter_candidates(const uint8_t* __restrict__ keep, const int64_t* __restrict__ pos, int64_t V,
+                                   int32_t* __restrict__ cand) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    if (keep[i]) cand[pos[i]] = (int32_t)i;
+}
+
+static inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+static inline int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
+
+static uint64_t g_sg_table_ready = 0;
+static cudaError_t ensure_sg_table() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && (g_sg_table_ready >> dev) & 1) return cudaSuccess;
+  PcgJump tab[64];
+  pcg_jump_table(tab, 64);
+  e = cudaMemcpyToSymbol(c_pow2_sg, tab, sizeof(tab));
+  if (e == cudaSuccess && dev < 64) g_sg_table_ready |= (1ull << dev);
+  return e;
+}
+
+// dispatch helper: (T, EPC, MAXC) from (precision, d)
+template <template <typename, int, int> class F, typename... Args>
+static int dispatch_rows(int precision, int d, Args&&... args) {
+  if (precision == WV_FP32) {
+    if (d % 4 == 0) {
+      const int C = d / 4;
+      if (C <= 32) return F<float, 4, 1>::run(args...);
+      if (C <= 64) return F<float, 4, 2>::run(args...);
+      if (C <= 128) return F<float, 4, 4>::run(args...);
+      if (C <= 256) return F<float, 4, 8>::run(args...);
+    } else {
+      if (d <= 32) return F<float, 1, 1>::run(args...);
+      if (d <= 64) return F<float, 1, 2>::run(args...);
+      if (d <= 128) return F<float, 1, 4>::run(args...);
+      if (d <= 256) return F<float, 1, 8>::run(args...);
+    }
+  } else if (precision == WV_FP64) {
+    if (d % 2 == 0) {
+      const int C = d / 2;
+      if (C <= 32) return F<double, 2, 1>::run(args...);
+      if (C <= 64) return F<double, 2, 2>::run(args...);
+      if (C <= 128) return F<double, 2, 4>::run(args...);
+      if (C <= 256) return F<double, 2, 8>::run(args...);
+    } else {
+      if (d <= 32) return F<double, 1, 1>::run(args...);
+      if (d <= 64) return F<double, 1, 2>::run(args...);
+      if (d <= 128) return F<double, 1, 4>::run(args...);
+      if (d <= 256) return F<double, 1, 8>::run(args...);
+    }
+  }
+  set_error("unsupported precision %d / vector_size %d", precision, d);
+  return -1;
+}
+
+template <typename T, int EPC, int MAXC>
+struct LaunchPair {
+  static int run(const PairArgs& a, const void* in, const void* out, unsigned grid, cudaStream_t st) {
+    sgns_pair_kernel<T, EPC, MAXC><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+};
+
+template <typename T, int EPC, int MAXC>
+struct LaunchOwner {
+  static int run(const OwnerArgs& a, unsigned grid, cudaStream_t st) {
+    sgns_owner_kernel<T, EPC, MAXC><<<grid, kOwnerThreads, 0, st>>>(a);
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+};
+
+}  // namespace wv
+
+extern "C" {
+
+int wv_sgns_init(int64_t vocab_size, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
+                 void* input_matrix, void* output_matrix, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(vocab_size >= 1 && vector_size >= 1, "bad sizes");
+  WV_CHECK_ARG(precision == WV_FP32 || precision == WV_FP64, "bad precision");
+  WV_CUDA(ensure_sg_table());
+  uint32_t pool[4];
+  ss_pool(seed_prefix, n_prefix - 1, seed_prefix[n_prefix - 1], pool);
+  Pcg64 g = pcg_seed(pool);
+  InitStream s{g.state, g.inc};
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int mtx = 0; mtx < 2; ++mtx) {
+    void* dst = mtx == 0 ? input_matrix : output_matrix;
+    if (precision == WV_FP32)
+      init_rows<float><<<grid_for(vocab_size, 128), 128, 0, st>>>(s, vocab_size, vector_size, 0, vocab_size, mtx,
+                                                                  (float*)dst, nullptr, nullptr);
+    else
+      init_rows<double><<<grid_for(vocab_size, 128), 128, 0, st>>>(s, vocab_size, vector_size, 0, vocab_size, mtx,
+                                                                   nullptr, nullptr, (double*)dst);
+    WV_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+// float64 export of one matrix (0 = input, 1 = output): modified rows are
+// cast from the parameter store, all others are regenerated bit-exactly
+// from the init stream (so untouched rows equal init_embeddings exactly).
+int wv_sgns_export(int64_t vocab_size, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
+                   int matrix, const void* params, const uint8_t* modified, double* out64, void* stream) {
+  using namespace wv;
+  WV_CUDA(ensure_sg_table());
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = vocab_size * (int64_t)vector_size;
+  if (precision == WV_FP64) {
+    WV_CUDA(cudaMemcpyAsync(out64, params, n * 8, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  export_rows<float><<<grid_for(n, 256), 256, 0, st>>>((const float*)params, n, out64);
+  WV_LAUNCH_CHECK();
+  uint32_t pool[4];
+  ss_pool(seed_prefix, n_prefix - 1, seed_prefix[n_prefix - 1], pool);
+  Pcg64 g = pcg_seed(pool);
+  InitStream s{g.state, g.inc};
+  init_rows<float><<<grid_for(vocab_size, 128), 128, 0, st>>>(s, vocab_size, vector_size, 0, vocab_size, matrix,
+                                                              nullptr, modified, out64);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int64_t wv_pair_index_workspace_bytes(int64_t n_walks) {
+  using namespace wv;
+  return al256(n_walks * 4) * 2 + al256(radix_ws_bytes(n_walks, 32)) + al256(n_walks) + al256((n_walks + 1) * 8) * 2 +
+         al256(scan_tiles(n_walks + 1) * 8) + 1024;
+}
+
+// Length-class index of a flat corpus for O(1) pair decode:
+// walks_by_class (stable by length), class_len/class_walk_start/class_pair_start
+// (each sized n_walks+1 by the caller), *n_classes and *n_pairs (device int64).
+int wv_pair_index_build(const int64_t* offsets, int64_t n_walks, int window, int32_t* walks_by_class,
+                        int64_t* class_len, int64_t* class_walk_start, int64_t* class_pair_start, int64_t* n_classes,
+                        int64_t* n_pairs, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(window >= 1, "window must be >= 1");
+  WV_CHECK_ARG(n_walks >= 1 && n_walks < (1ll << 31), "bad walk count");
+  WV_CHECK_ARG(ws_bytes >= wv_pair_index_workspace_bytes(n_walks), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  uint32_t* keys = (uint32_t*)w;
+  w += al256(n_walks * 4);
+  uint32_t* vals = (uint32_t*)walks_by_class;
+  uint32_t* tmpv = (uint32_t*)w;
+  w += al256(n_walks * 4);
+  void* rws = w;
+  w += al256(radix_ws_bytes(n_walks, 32));
+  uint8_t* head = (uint8_t*)w;
+  w += al256(n_walks);
+  int64_t* cls = (int64_t*)w;
+  w += al256((n_walks + 1) * 8);
+  int64_t* cpairs = (int64_t*)w;
+  w += al256((n_walks + 1) * 8);
+  int64_t* scan_ws = (int64_t*)w;
+  (void)tmpv;
+  walk_len_keys<<<grid_for(n_walks, 256), 256, 0, st>>>(offsets, n_walks, keys, vals);
+  WV_LAUNCH_CHECK();
+  WV_CUDA(radix_sort_pairs(keys, vals, n_walks, 32, rws, st));
+  class_heads<<<grid_for(n_walks, 256), 256, 0, st>>>(keys, n_walks, head);
+  WV_LAUNCH_CHECK();
+  WV_CUDA((excl_scan<uint8_t, int64_t>(head, n_walks, cls, n_classes, scan_ws, st)));
+  class_fill<<<grid_for(n_walks, 256), 256, 0, st>>>(keys, n_walks, head, cls, class_len, class_walk_start);
+  WV_CUDA(cudaMemsetAsync(cpairs, 0, n_walks * 8, st));
+  class_pairs<<<grid_for(n_walks, 256), 256, 0, st>>>(class_len, class_walk_start, n_classes, n_walks, window,
+                                                       cpairs);
+  WV_LAUNCH_CHECK();
+  // class_pair_start = exclusive scan over the (n_classes) entries; entries
+  // past n_classes are never read (the kernel is bounded by n_classes).
+  WV_CUDA((excl_scan<int64_t, int64_t>(cpairs, n_walks, class_pair_start, n_pairs, scan_ws, st)));
+  return 0;
+}
+
+int64_t wv_pairs_workspace_bytes(int64_t n_walks) {
+  using namespace wv;
+  return al256(n_walks * 8) * 2 + al256(scan_tiles(n_walks) * 8) + al256(8) + 256;
+}
+
+// Reference-order (N,2) pair table (generate_pairs, w2v.py:161-191).  The
+// caller sizes `pairs` from wv_pair_index_build's n_pairs.
+int wv_generate_pairs(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int window, int32_t* pairs,
+                      int64_t* n_pairs_out, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(ws_bytes >= wv_pairs_workspace_bytes(n_walks), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int64_t* cnt = (int64_t*)w;
+  w += al256(n_walks * 8);
+  int64_t* prefix = (int64_t*)w;
+  w += al256(n_walks * 8);
+  int64_t* scan_ws = (int64_t*)w;
+  w += al256(scan_tiles(n_walks) * 8);
+  int64_t* n_s = (int64_t*)w;
+  // host needs block bases; shift counts are read back synchronously
+  int64_t base = 0;
+  for (int s = 1; s <= window; ++s) {
+    pairs_per_walk<<<grid_for(n_walks, 256), 256, 0, st>>>(offsets, n_walks, s, cnt);
+    WV_LAUNCH_CHECK();
+    WV_CUDA((excl_scan<int64_t, int64_t>(cnt, n_walks, prefix, n_s, scan_ws, st)));
+    int64_t ns_host = 0;
+    WV_CUDA(cudaMemcpyAsync(&ns_host, n_s, 8, cudaMemcpyDeviceToHost, st));
+    WV_CUDA(cudaStreamSynchronize(st));
+    if (ns_host == 0) break;
+    if (pairs)
+      pairs_emit<<<grid_for(n_walks, 128), 128, 0, st>>>(tokens, offsets, n_walks, s, prefix, n_s, base, pairs);
+    WV_LAUNCH_CHECK();
+    base += 2 * ns_host;
+  }
+  *n_pairs_out = base;
+  return 0;
+}
+
+int64_t wv_candidates_workspace_bytes(int64_t vocab_size) {
+  using namespace wv;
+  return al256(vocab_size) + al256(vocab_size * 8) + al256(scan_tiles(vocab_size) * 8) + 256;
+}
+
+// candidates = flatnonzero(freq >= min_count) (w2v.py:525-526); keep mask out.
+int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, uint8_t* keep, int32_t* candidates,
+                  int64_t* n_candidates, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(ws_bytes >= wv_candidates_workspace_bytes(vocab_size), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  w += al256(vocab_size);
+  int64_t* pos = (int64_t*)w;
+  w += al256(vocab_size * 8);
+  int64_t* scan_ws = (int64_t*)w;
+  flags_to_candidates<<<grid_for(vocab_size, 256), 256, 0, st>>>(freq, vocab_size, min_count, keep);
+  WV_LAUNCH_CHECK();
+  WV_CUDA((excl_scan<uint8_t, int64_t>(keep, vocab_size, pos, n_candidates, scan_ws, st)));
+  scatter_candidates<<<grid_for(vocab_size, 256), 256, 0, st>>>(keep, pos, vocab_size, candidates);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, void* stream) {
+  using namespace wv;
+  state_reset_epoch<<<1, 1, 0, (cudaStream_t)stream>>>(state, epoch, start);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
+                                      int precision) {
+  using namespace wv;
+  const int64_t es = precision == WV_FP64 ? 8 : 4;
+  const int64_t items = batch * (2 + negatives);
+  const int bits = bits_for((uint64_t)(2 * vocab_size - 1));
+  return al256(batch * vector_size * es) * 2 + al256(batch * (negatives + 1) * es) + al256(items * 4) * 2 +
+         al256(radix_ws_bytes(items, bits)) + al256(items * 8) + al256(148 * 32 * 8) + al256(64) + 1024;
+}
+
+// One SGNS batch: pair phase -> stable grouping sort -> owner Adam phase.
+// Every launch is stream-ordered and reads the batch cursor from `state`, so
+// the sequence is CUDA-graph capturable and replayable.
+int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream) {
+  return wv_sgns_batch_phases(model, batch, ws, ws_bytes, WV_PHASE_ALL, stream);
+}
+
+// The batch split into its three phases (pair gather / grouping sort /
+// owner update) so callers can bracket each with events; all state flows
+// through the workspace, so calling the phases in order equals one batch.
+int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int phases,
+                         void* stream) {
+  using namespace wv;
+  const int64_t V = model->vocab_size;
+  const int d = model->vector_size;
+  const int k = batch->negatives;
+  const int64_t B = batch->batch_rows;
+  WV_CHECK_ARG(B >= 1, "empty batch");
+  WV_CHECK_ARG(2 * V < (int64_t)0xffffffffLL, "vocabulary too large for 32-bit sort keys");
+  WV_CHECK_ARG(B * (2 + k) < (int64_t)0xffffffffLL, "batch too large");
+  WV_CHECK_ARG(ws_bytes >= wv_sgns_batch_workspace_bytes(V, d, k, B, model->precision), "workspace too small");
+  WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t es = model->precision == WV_FP64 ? 8 : 4;
+  const int64_t items = B * (2 + k);
+  const int bits = bits_for((uint64_t)(2 * V - 1));
+  char* w = (char*)ws;
+  void* U = w;
+  w += al256(B * d * es);
+  void* G = w;
+  w += al256(B * d * es);
+  void* coef = w;
+  w += al256(B * (k + 1) * es);
+  uint32_t* keys = (uint32_t*)w;
+  w += al256(items * 4);
+  uint32_t* vals = (uint32_t*)w;
+  w += al256(items * 4);
+  void* rws = w;
+  w += al256(radix_ws_bytes(items, bits));
+  int64_t* seg_start = (int64_t*)w;
+  w += al256(items * 8);
+  double* partials = (double*)w;
+  w += al256(148 * 32 * 8);
+  uint32_t* seg_count = (uint32_t*)w;
+
+  PairArgs pa;
+  pa.mode = batch->mode;
+  pa.V = V;
+  pa.d = d;
+  pa.k = k;
+  pa.window = batch->window;
+  pa.B = B;
+  pa.N = batch->n_pairs;
+  pa.seed = batch->seed;
+  pa.tokens = batch->tokens;
+  pa.offsets = batch->offsets;
+  pa.class_len = batch->class_len;
+  pa.class_pair_start = batch->class_pair_start;
+  pa.class_walk_start = batch->class_walk_start;
+  pa.n_classes = (int)batch->n_classes;
+  pa.walks_by_class = batch->walks_by_class;
+  pa.candidates = batch->candidates;
+  pa.n_candidates = batch->n_candidates;
+  pa.pairs = batch->pairs;
+  pa.perm = batch->perm;
+  pa.negatives = batch->negative_table;
+  pa.U = U;
+  pa.G = G;
+  pa.coef = coef;
+  pa.keys = keys;
+  pa.vals = vals;
+  pa.partials = partials;
+  pa.state = model->state;
+  pa.seg_count = seg_count;
+  const unsigned pgrid = grid_for(B, kPairWarps, 148 * 32);
+  int rc = 0;
+  if (phases & WV_PHASE_PAIRS) {
+    rc = dispatch_rows<LaunchPair>(model->precision, d, pa, (const void*)model->input, (const void*)model->output,
+                                   pgrid, st);
+    if (rc) return rc;
+  }
+  if (phases & WV_PHASE_GROUP) {
+    WV_CUDA(radix_sort_pairs(keys, vals, items, bits, rws, st));
+    seg_heads<<<grid_for(items, 256), 256, 0, st>>>(keys, items, seg_start, seg_count, model->state, B);
+    WV_LAUNCH_CHECK();
+  }
+  if (!(phases & WV_PHASE_UPDATE)) return 0;
+  OwnerArgs oa;
+  oa.V = V;
+  oa.d = d;
+  oa.k = k;
+  oa.B = B;
+  oa.n_items = items;
+  oa.keys = keys;
+  oa.vals = vals;
+  oa.seg_start = seg_start;
+  oa.seg_count = seg_count;
+  oa.U = U;
+  oa.G = G;
+  oa.coef = coef;
+  oa.in = model->input;
+  oa.out = model->output;
+  oa.m_in = model->m_in;
+  oa.v_in = model->v_in;
+  oa.m_out = model->m_out;
+  oa.v_out = model->v_out;
+  oa.steps_in = model->steps_in;
+  oa.steps_out = model->steps_out;
+  oa.touched_in = model->touched_in;
+  oa.touched_out = model->touched_out;
+  oa.modified_in = model->modified_in;
+  oa.modified_out = model->modified_out;
+  oa.lr = model->learning_rate;
+  oa.sparse = model->sparse;
+  oa.dense_g_in = model->dense_g_in;
+  oa.dense_g_out = model->dense_g_out;
+  oa.state = model->state;
+  const unsigned ogrid = grid_for(items, kOwnerThreads / 32, 148 * 16);
+  rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, ogrid, st);
+  if (rc) return rc;
+  if (!model->sparse) {
+    const int64_t n = V * (int64_t)d;
+    if (model->precision == WV_FP32) {
+      dense_adam<float><<<grid_for(n, 256), 256, 0, st>>>((float*)model->input, (float*)model->m_in,
+                                                          (float*)model->v_in, (float*)model->dense_g_in, n, d,
+                                                          model->state, model->learning_rate, model->modified_in);
+      dense_adam<float><<<grid_for(n, 256), 256, 0, st>>>((float*)model->output, (float*)model->m_out,
+                                                          (float*)model->v_out, (float*)model->dense_g_out, n, d,
+                                                          model->state, model->learning_rate, model->modified_out);
+    } else {
+      dense_adam<double><<<grid_for(n, 256), 256, 0, st>>>((double*)model->input, (double*)model->m_in,
+                                                           (double*)model->v_in, (double*)model->dense_g_in, n, d,
+                                                           model->state, model->learning_rate, model->modified_in);
+      dense_adam<double><<<grid_for(n, 256), 256, 0, st>>>((double*)model->output, (double*)model->m_out,
+                                                           (double*)model->v_out, (double*)model->dense_g_out, n, d,
+                                                           model->state, model->learning_rate, model->modified_out);
+    }
+    WV_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,435 @@
+// Walk-corpus kernels: uniform random walks (one walker per lane), the
+// fixed-width -> flat compaction, duplicate-free filtering per root group,
+// entity/property projections, token histogram and min_count filtering.
+//
+// Reference (pkg/src/walkvec/walks.py):
+//   random_walks      :144-204  work list = repeat(roots, walk_number) (:166),
+//                               8192-item shards, one numpy stream per shard
+//                               seeded SeedSequence([seed, 0, shard]) (:168-173)
+//   _walk_shard       :117-141  per hop: deg = off[cur+1]-off[cur]; alive &= deg>0;
+//                               draw = rng.random(n) (one per row, alive or not);
+//                               pick = min(int(draw*deg), deg-1) in float64
+//   duplicate_free    :186-202  keep first occurrence per root group
+//   project_corpus    :323-341
+// The draw for (shard s, hop h, row i) is stream element k = h*n_s + i, so a
+// walker addresses it directly: PCG64 by affine jump-ahead, Philox by counter.
+#include "common.cuh"
+#include "primitives.cuh"
+#include "../../include/walkvec_b200.h"
+
+namespace wv {
+
+constexpr int kShard = 8192;  // walks.py:34 SHARD_SIZE
+constexpr int kWalkThreads = 256;
+
+// PCG64 jump table: entry b advances 2^b steps (multiplier-only, so shared).
+__constant__ PcgJump c_pcg_pow2[64];
+static uint64_t g_pcg_table_ready = 0;  // bit per device
+
+static cudaError_t ensure_pcg_table() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && (g_pcg_table_ready >> dev) & 1) return cudaSuccess;
+  PcgJump tab[64];
+  pcg_jump_table(tab, 64);
+  e = cudaMemcpyToSymbol(c_pcg_pow2, tab, sizeof(tab));
+  if (e == cudaSuccess && dev < 64) g_pcg_table_ready |= (1ull << dev);
+  return e;
+}
+
+__device__ __forceinline__ PcgJump pcg_jump_dev(uint64_t n) {
+  PcgJump r{u128{1, 0}, u128{0, 0}};
+  for (int b = 0; n; ++b, n >>= 1)
+    if (n & 1) r = jump_compose(r, c_pcg_pow2[b]);
+  return r;
+}
+
+struct WalkParams {
+  const int64_t* row_offsets;
+  const uint64_t* edges;
+  const int64_t* roots;
+  int64_t walk_number;
+  int64_t work_begin;  // global index of the first walker of this launch
+  int64_t work_count;  // walkers in this launch
+  int64_t last_shard;  // global shard index of the final (possibly partial) shard
+  int64_t n_last;      // its row count
+  int depth;
+  int width;
+  int n_prefix;
+  uint32_t prefix[13];
+  PcgJump stride_full;  // 8192 steps
+  PcgJump stride_last;  // n_last steps
+  int32_t* corpus;
+  int32_t* lengths;
+};
+
+template <int RNG>
+__global__ void __launch_bounds__(kWalkThreads) random_walk_kernel(WalkParams P) {
+  extern __shared__ int32_t stage[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int width = P.width;
+  const int64_t wl = blockIdx.x * (int64_t)kWalkThreads + threadIdx.x;
+  int32_t* my = stage + (warp * 32 + lane) * width;
+  for (int j = 0; j < width; ++j) my[j] = -1;
+  int len = 0;
+  if (wl < P.work_count) {
+    const int64_t w = P.work_begin + wl;
+    const int64_t s = w / kShard;
+    const uint64_t i = (uint64_t)(w - s * kShard);
+    const bool last = (s == P.last_shard);
+    const uint64_t n_s = last ? (uint64_t)P.n_last : (uint64_t)kShard;
+    int64_t cur = P.roots[w / P.walk_number];
+    my[0] = (int32_t)cur;
+    len = 1;
+    uint32_t pool[4];
+    ss_pool(P.prefix, P.n_prefix, (uint64_t)s, pool);
+    u128 x{0, 0}, cstep{0, 0};
+    u128 astep{1, 0};
+    uint64_t k0 = 0, k1 = 0;
+    if (RNG == WV_RNG_PCG64) {
+      Pcg64 g = pcg_seed(pool);
+      PcgJump j = pcg_jump_dev(i + 1);
+      x = add128(mul128(j.A, g.state), mul128(g.inc, j.S));
+      const PcgJump& st = last ? P.stride_last : P.stride_full;
+      astep = st.A;
+      cstep = mul128(g.inc, st.S);
+    } else {
+      uint64_t key[2];
+      ss_generate_u64(pool, 2, key);
+      k0 = key[0];
+      k1 = key[1];
+    }
+    const int64_t* __restrict__ off = P.row_offsets;
+    const uint64_t* __restrict__ edges = P.edges;
+    for (int h = 0; h < P.depth; ++h) {
+      const int64_t lo = __ldg(off + cur), hi = __ldg(off + cur + 1);
+      if (hi == lo) break;
+      uint64_t u;
+      if (RNG == WV_RNG_PCG64) {
+        u = pcg_output(x);
+        x = add128(mul128(astep, x), cstep);
+      } else {
+        u = philox_numpy_u64(k0, k1, (uint64_t)h * n_s + i);
+      }
+      const int64_t deg = hi - lo;
+      int64_t pick = __double2ll_rz(__dmul_rn(u64_to_double(u), (double)deg));
+      if (pick > deg - 1) pick = deg - 1;
+      const uint64_t e = __ldg(edges + lo + pick);
+      my[2 * h + 1] = (int32_t)(e >> 32);
+      my[2 * h + 2] = (int32_t)(uint32_t)e;
+      cur = (int64_t)(uint32_t)e;
+      len += 2;
+    }
+    P.lengths[wl] = len;
+  }
+  __syncwarp();
+  const int64_t wl0 = wl - lane;
+  if (wl0 >= P.work_count) return;
+  const int64_t nvalid = min((int64_t)32, P.work_count - wl0);
+  const int32_t* src = stage + warp * 32 * width;
+  int32_t* dst = P.corpus + wl0 * width;
+  const int total = (int)nvalid * width;
+  if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    const int4* s4 = reinterpret_cast<const int4*>(src);
+    int4* d4 = reinterpret_cast<int4*>(dst);
+    for (int j = lane; j < total / 4; j += 32) d4[j] = s4[j];
+  } else {
+    for (int j = lane; j < total; j += 32) dst[j] = src[j];
+  }
+}
+
+// ---------------------------------------------------------- compaction ----
+template <typename TokOut>
+__global__ void compact_rows(const int32_t* __restrict__ corpus, const int32_t* __restrict__ lengths,
+                             int64_t n_walks, int width, const int64_t* __restrict__ offsets,
+                             TokOut* __restrict__ tokens) {
+  const int64_t total = n_walks * width;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = idx / width;
+    const int j = (int)(idx - w * width);
+    if (j < lengths[w]) tokens[offsets[w] + j] = (TokOut)corpus[idx];
+  }
+}
+
+__global__ void set_last_offset(int64_t* offsets, int64_t n, const int64_t* total) { offsets[n] = *total; }
+
+// ----------------------------------------------------- duplicate-free ----
+__global__ void row_hash(const int32_t* __restrict__ corpus, const int32_t* __restrict__ lengths, int64_t n_walks,
+                         int width, uint64_t* __restrict__ hash) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    const int L = lengths[w];
+    uint64_t h = splitmix64((uint64_t)L);
+    for (int j = 0; j < L; ++j) h = splitmix64(h ^ (uint64_t)(uint32_t)corpus[w * width + j]);
+    hash[w] = h;
+  }
+}
+
+__global__ void first_occurrence(const int32_t* __restrict__ corpus, const int32_t* __restrict__ lengths,
+                                 int64_t n_walks, int width, int64_t group, const uint64_t* __restrict__ hash,
+                                 uint8_t* __restrict__ keep) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g0 = (w / group) * group;
+    const uint64_t h = hash[w];
+    const int L = lengths[w];
+    bool first = true;
+    for (int64_t q = g0; q < w && first; ++q) {
+      if (hash[q] != h || lengths[q] != L) continue;
+      bool same = true;
+      for (int j = 0; j < L && same; ++j) same = corpus[q * width + j] == corpus[w * width + j];
+      if (same) first = false;
+    }
+    keep[w] = first ? 1 : 0;
+  }
+}
+
+__global__ void masked_lengths(const int32_t* __restrict__ lengths, const uint8_t* __restrict__ keep,
+                               int64_t n, int32_t* __restrict__ out) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x)
+    out[w] = keep[w] ? lengths[w] : 0;
+}
+
+__global__ void gather_kept_rows(const int32_t* __restrict__ corpus, const int32_t* __restrict__ lengths,
+                                 const uint8_t* __restrict__ keep, const int64_t* __restrict__ new_index,
+                                 int64_t n_walks, int width, int32_t* __restrict__ out_corpus,
+                                 int32_t* __restrict__ out_lengths) {
+  const int64_t total = n_walks * width;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = idx / width;
+    if (!keep[w]) continue;
+    const int j = (int)(idx - w * width);
+    const int64_t nw = new_index[w];
+    out_corpus[nw * width + j] = corpus[idx];
+    if (j == 0) out_lengths[nw] = lengths[w];
+  }
+}
+
+// ------------------------------------------------ flat-corpus filtering ----
+// mode: WV_KEEP_ENTITY (even positions), WV_KEEP_PROPERTY (0 + odd positions),
+//       WV_KEEP_TOKENS (token mask, min_count filter; w2v.py:146-158)
+__device__ __forceinline__ bool keep_pos(int mode, int64_t pos, int32_t tok, const uint8_t* mask) {
+  if (mode == WV_KEEP_ENTITY) return (pos & 1) == 0;
+  if (mode == WV_KEEP_PROPERTY) return pos == 0 || (pos & 1) == 1;
+  return mask[tok] != 0;
+}
+
+__global__ void filter_count(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets, int64_t n_walks,
+                             int mode, const uint8_t* __restrict__ mask, int64_t* __restrict__ kept) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    for (int64_t p = offsets[w]; p < offsets[w + 1]; ++p) c += keep_pos(mode, p - offsets[w], tokens[p], mask);
+    kept[w] = c;
+  }
+}
+
+__global__ void filter_scatter(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets, int64_t n_walks,
+                               int mode, const uint8_t* __restrict__ mask, const int64_t* __restrict__ new_offsets,
+                               int32_t* __restrict__ out) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = new_offsets[w];
+    for (int64_t p = offsets[w]; p < offsets[w + 1]; ++p) {
+      const int32_t t = tokens[p];
+      if (keep_pos(mode, p - offsets[w], t, mask)) out[o++] = t;
+    }
+  }
+}
+
+// ------------------------------------------------------------ histogram ----
+// Warp-aggregated: lanes holding the same token (hot predicate rows) merge
+// into one atomic.
+__global__ void token_hist(const int32_t* __restrict__ tokens, int64_t n, unsigned long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t t = i < n ? tokens[i] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, t);
+    if (t >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&counts[t], (unsigned long long)__popc(peers));
+  }
+}
+
+static inline unsigned grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+static inline int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
+
+}  // namespace wv
+
+extern "C" {
+
+int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
+                    const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth,
+                    int64_t work_begin, int64_t work_count, const uint32_t* seed_prefix, int n_prefix, int rng_kind,
+                    int32_t* corpus, int32_t* lengths, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(walk_depth >= 1, "walk_depth must be >= 1");
+  WV_CHECK_ARG(walk_number >= 1, "walk_number must be >= 1");
+  WV_CHECK_ARG(n_roots >= 1, "start_vertices must be non-empty");
+  WV_CHECK_ARG(vertex_count >= 1, "empty graph");
+  WV_CHECK_ARG(n_prefix >= 0 && n_prefix <= 13, "seed prefix too long");
+  WV_CHECK_ARG(rng_kind == WV_RNG_PCG64 || rng_kind == WV_RNG_PHILOX, "unknown rng kind %d", rng_kind);
+  const int64_t total = n_roots * walk_number;
+  WV_CHECK_ARG(work_begin >= 0 && work_count >= 0 && work_begin + work_count <= total, "work range out of bounds");
+  const int width = 2 * walk_depth + 1;
+  WV_CHECK_ARG((int64_t)kWalkThreads * width * 4 <= 227 * 1024, "walk_depth %d exceeds the staged-row limit (110)",
+               walk_depth);
+  if (work_count == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  WV_CUDA(ensure_pcg_table());
+  WalkParams P;
+  P.row_offsets = row_offsets;
+  P.edges = packed_edges;
+  P.roots = roots;
+  P.walk_number = walk_number;
+  P.work_begin = work_begin;
+  P.work_count = work_count;
+  P.last_shard = (total - 1) / kShard;
+  P.n_last = total - P.last_shard * kShard;
+  P.depth = walk_depth;
+  P.width = width;
+  P.n_prefix = n_prefix;
+  for (int i = 0; i < n_prefix; ++i) P.prefix[i] = seed_prefix[i];
+  PcgJump tab[64];
+  pcg_jump_table(tab, 64);
+  P.stride_full = pcg_jump_n(tab, kShard);
+  P.stride_last = pcg_jump_n(tab, (uint64_t)P.n_last);
+  P.corpus = corpus;
+  P.lengths = lengths;
+  const size_t smem = (size_t)kWalkThreads * width * sizeof(int32_t);
+  const int64_t blocks = (work_count + kWalkThreads - 1) / kWalkThreads;
+  WV_CHECK_ARG(blocks < (1ll << 31), "too many walkers for one launch");
+  if (rng_kind == WV_RNG_PCG64) {
+    if (smem > 48 * 1024)
+      WV_CUDA(cudaFuncSetAttribute(random_walk_kernel<WV_RNG_PCG64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    random_walk_kernel<WV_RNG_PCG64><<<(unsigned)blocks, kWalkThreads, smem, st>>>(P);
+  } else {
+    if (smem > 48 * 1024)
+      WV_CUDA(cudaFuncSetAttribute(random_walk_kernel<WV_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    random_walk_kernel<WV_RNG_PHILOX><<<(unsigned)blocks, kWalkThreads, smem, st>>>(P);
+  }
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int64_t wv_compact_workspace_bytes(int64_t n_walks) {
+  using namespace wv;
+  return al256(scan_tiles(n_walks + 1) * 8) + al256(8) + 256;
+}
+
+int wv_corpus_compact(const int32_t* corpus, const int32_t* lengths, int64_t n_walks, int width,
+                      int64_t* offsets, void* tokens, int token_bytes, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(token_bytes == 4 || token_bytes == 8, "token_bytes must be 4 or 8");
+  WV_CHECK_ARG(ws_bytes >= wv_compact_workspace_bytes(n_walks), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int64_t* scan_ws = (int64_t*)w;
+  w += al256(scan_tiles(n_walks + 1) * 8);
+  int64_t* total = (int64_t*)w;
+  WV_CUDA((excl_scan<int32_t, int64_t>(lengths, n_walks, offsets, total, scan_ws, st)));
+  set_last_offset<<<1, 1, 0, st>>>(offsets, n_walks, total);
+  WV_LAUNCH_CHECK();
+  if (n_walks == 0) return 0;
+  const int64_t cells = n_walks * width;
+  if (token_bytes == 4)
+    compact_rows<int32_t><<<grid_for(cells, 256), 256, 0, st>>>(corpus, lengths, n_walks, width, offsets,
+                                                                 (int32_t*)tokens);
+  else
+    compact_rows<int64_t><<<grid_for(cells, 256), 256, 0, st>>>(corpus, lengths, n_walks, width, offsets,
+                                                                 (int64_t*)tokens);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int64_t wv_dedup_workspace_bytes(int64_t n_walks) {
+  using namespace wv;
+  return al256(n_walks * 8) * 2 + al256(n_walks) + al256(scan_tiles(n_walks) * 8) + al256(8) + 256;
+}
+
+// Duplicate-free (walks.py:186-202): within each group of `group` consecutive
+// walks keep the first occurrence of each distinct token sequence.  Writes
+// the kept rows (in order) to out_corpus/out_lengths and their count to
+// *n_kept (device int64).
+int wv_duplicate_free(const int32_t* corpus, const int32_t* lengths, int64_t n_walks, int width, int64_t group,
+                      int32_t* out_corpus, int32_t* out_lengths, int64_t* n_kept, void* ws, int64_t ws_bytes,
+                      void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(group >= 1, "group must be >= 1");
+  WV_CHECK_ARG(ws_bytes >= wv_dedup_workspace_bytes(n_walks), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_walks == 0) {
+    WV_CUDA(cudaMemsetAsync(n_kept, 0, 8, st));
+    return 0;
+  }
+  char* w = (char*)ws;
+  uint64_t* hash = (uint64_t*)w;
+  w += al256(n_walks * 8);
+  int64_t* new_index = (int64_t*)w;
+  w += al256(n_walks * 8);
+  uint8_t* keep = (uint8_t*)w;
+  w += al256(n_walks);
+  int64_t* scan_ws = (int64_t*)w;
+  row_hash<<<grid_for(n_walks, 256), 256, 0, st>>>(corpus, lengths, n_walks, width, hash);
+  first_occurrence<<<grid_for(n_walks, 128), 128, 0, st>>>(corpus, lengths, n_walks, width, group, hash, keep);
+  WV_LAUNCH_CHECK();
+  WV_CUDA((excl_scan<uint8_t, int64_t>(keep, n_walks, new_index, n_kept, scan_ws, st)));
+  gather_kept_rows<<<grid_for(n_walks * width, 256), 256, 0, st>>>(corpus, lengths, keep, new_index, n_walks, width,
+                                                                     out_corpus, out_lengths);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int64_t wv_filter_workspace_bytes(int64_t n_walks) {
+  using namespace wv;
+  return al256((n_walks + 1) * 8) + al256(scan_tiles(n_walks + 1) * 8) + al256(8) + 256;
+}
+
+// Flat corpus filter: per-walk keep predicate -> new offsets (n_walks+1) and
+// tokens.  Walk count is preserved (empty walks stay, as in the reference).
+int wv_corpus_filter(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int mode,
+                     const uint8_t* token_mask, int64_t* new_offsets, int32_t* new_tokens, void* ws, int64_t ws_bytes,
+                     void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(mode == WV_KEEP_ENTITY || mode == WV_KEEP_PROPERTY || mode == WV_KEEP_TOKENS, "bad filter mode");
+  WV_CHECK_ARG(mode != WV_KEEP_TOKENS || token_mask != nullptr, "token mask required");
+  WV_CHECK_ARG(ws_bytes >= wv_filter_workspace_bytes(n_walks), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int64_t* kept = (int64_t*)w;
+  w += al256((n_walks + 1) * 8);
+  int64_t* scan_ws = (int64_t*)w;
+  w += al256(scan_tiles(n_walks + 1) * 8);
+  int64_t* total = (int64_t*)w;
+  if (n_walks > 0) {
+    filter_count<<<grid_for(n_walks, 256), 256, 0, st>>>(tokens, offsets, n_walks, mode, token_mask, kept);
+    WV_LAUNCH_CHECK();
+  }
+  WV_CUDA((excl_scan<int64_t, int64_t>(kept, n_walks, new_offsets, total, scan_ws, st)));
+  set_last_offset<<<1, 1, 0, st>>>(new_offsets, n_walks, total);
+  if (n_walks > 0)
+    filter_scatter<<<grid_for(n_walks, 256), 256, 0, st>>>(tokens, offsets, n_walks, mode, token_mask, new_offsets,
+                                                           new_tokens);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int wv_token_histogram(const int32_t* tokens, int64_t n_tokens, int64_t vocab_size, int64_t* counts, int zero_first,
+                       void* stream) {
+  using namespace wv;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (zero_first) WV_CUDA(cudaMemsetAsync(counts, 0, vocab_size * 8, st));
+  if (n_tokens == 0) return 0;
+  token_hist<<<grid_for(n_tokens, 256), 256, 0, st>>>(tokens, n_tokens, (unsigned long long*)counts);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+"""Synthetic knowledge graphs of the benchmark shapes (vectorised, host numpy).
+
+Reference generators: pkg/src/walkvec/benchgen.py:78-161.
+  * gen_barabasi (:78-109): each new vertex v adds min(m, v) distinct edges
+    v -> t, t drawn from the attachment bag (every vertex once per unit of
+    degree + 1), so in-degree is power-law and out-degree is m.  The
+    reference is a sequential Python loop (35 s at 1M vertices); here the bag
+    draw is restated as position sampling + pointer jumping: a draw at bag
+    position q of an earlier edge's target slot takes that edge's target.
+    Same process, not the same numpy stream (stated in DESIGN.md).
+  * gen_erdos_renyi (:112-127): blocked Bernoulli matrix -- already vectorised
+    in the reference; the same stream consumption gives the same graph.
+  * assign_predicates (:152-161): i.i.d. uniform predicate per edge from
+    SeedSequence([seed, 3]) -- identical stream.
+Token encoding is ingest.encode_integer_triples (first occurrence order).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .ingest import encode_integer_triples
+
+
+def _gen_rng(seed: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence([int(seed), 2]))
+
+
+def barabasi_edges(n: int, m: int, seed: int = 0) -> np.ndarray:
+    """(E,2) int64 (src, dst) preferential-attachment edges, vectorised."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    rng = _gen_rng(seed)
+    v = np.arange(1, n, dtype=np.int64)
+    k = np.minimum(m, v)                       # edges of vertex v
+    e_off = np.zeros(n, dtype=np.int64)        # first edge index of vertex v (v>=1 at e_off[v])
+    np.cumsum(k, out=e_off[1:])
+    E = int(e_off[-1])
+    src = np.repeat(v, k)
+    j = np.arange(E, dtype=np.int64) - e_off[src - 1]  # slot within the vertex
+    # bag length before vertex v: 1 + sum_{u<v} (2 k_u + 1)
+    bag_before = np.ones(n, dtype=np.int64)
+    bag_before[1:] += np.cumsum(2 * k + 1) - (2 * k + 1)
+    # bag position of vertex u's block start (u >= 1): bag_before[u]
+    L = bag_before[src]                        # draws of vertex v use positions [0, L)
+
+    def resolve(q):
+        # map bag position -> (kind, index): position 0 = vertex 0 self slot;
+        # block of u>=1 at bag_before[u]: [t1, u, t2, u, ..., tk, u, u]
+        u = np.searchsorted(bag_before, q, side="right") - 1
+        off = q - bag_before[u]
+        is_self0 = u == 0
+        in_pairs = (~is_self0) & (off < 2 * k[np.maximum(u, 1) - 1])
+        is_target = in_pairs & (off % 2 == 0)
+        edge = np.where(is_target, e_off[np.maximum(u, 1) - 1] + off // 2, -1)
+        return u, is_target, edge
+
+    q = (rng.random(E) * L).astype(np.int64)
+    tgt = np.full(E, -1, dtype=np.int64)
+    for _ in range(64):
+        u, is_t, edge = resolve(q)
+        val = np.where(is_t, -1, u)
+        ptr = edge.copy()
+        unresolved = is_t.copy()
+        # pointer jumping over target slots: value of edge e = value of the slot it drew
+        cur_val = val
+        cur_ptr = ptr
+        for _ in range(64):
+            if not unresolved.any():
+                break
+            nxt = cur_ptr[unresolved]
+            nv = cur_val[nxt]
+            np_ = cur_ptr[nxt]
+            idx = np.flatnonzero(unresolved)
+            cur_val = cur_val.copy()
+            cur_ptr = cur_ptr.copy()
+            cur_val[idx] = nv
+            cur_ptr[idx] = np_
+            unresolved = cur_val < 0
+        tgt = cur_val
+        # duplicate targets within a vertex are redrawn (the reference rejects them)
+        key = src * n + tgt
+        order = np.argsort(key, kind="stable")
+        dup_sorted = np.zeros(E, dtype=bool)
+        dup_sorted[1:] = key[order][1:] == key[order][:-1]
+        dup = np.zeros(E, dtype=bool)
+        dup[order] = dup_sorted
+        if not dup.any():
+            break
+        q[dup] = (rng.random(int(dup.sum())) * L[dup]).astype(np.int64)
+    del j
+    return np.column_stack([src, tgt])
+
+
+def erdos_renyi_edges(n: int, p: float, seed: int = 0) -> np.ndarray:
+    """Ordered pairs (u, v), u != v, each present with probability p (benchgen.py:112-127)."""
+    if not 0 < p < 1:
+        raise ValueError("p must be in (0, 1)")
+    rng = _gen_rng(seed)
+    rows_per_block = max(1, (1 << 24) // n)
+    chunks = []
+    for lo in range(0, n, rows_per_block):
+        hi = min(lo + rows_per_block, n)
+        rr, cc = np.nonzero(rng.random((hi - lo, n)) < p)
+        rr = rr + lo
+        keep = rr != cc
+        chunks.append(np.column_stack([rr[keep], cc[keep]]))
+    return np.vstack(chunks).astype(np.int64)
+
+
+def predicate_picks(n_edges: int, predicate_set_size: int, seed: int = 0) -> np.ndarray:
+    """assign_predicates' stream (benchgen.py:152-161): one uniform pick per edge."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 3]))
+    return rng.integers(0, predicate_set_size, size=n_edges)
+
+
+def synthetic_kg(model: str, n: int, m: int = 10, p: float = 0.001, predicates: int = 10, seed: int = 7):
+    """Token-encoded synthetic KG: (edges (E,3) int64, vocab_size, entity_tokens, predicate_tokens)."""
+    if model == "barabasi":
+        e2 = barabasi_edges(n, m, seed)
+    elif model == "erdos_renyi":
+        e2 = erdos_renyi_edges(n, p, seed)
+    else:
+        raise ValueError(f"unknown model {model!r}")
+    picks = predicate_picks(len(e2), predicates, seed)
+    return encode_integer_triples(e2[:, 0], picks, e2[:, 1], n)

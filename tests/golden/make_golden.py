@@ -1,0 +1,217 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container (the reference is importable read-only):
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+Writes tests/golden/*.npz / *.json.  The GPU box never needs /root/reference:
+tests read only these committed files.
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+from unittest import mock
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+
+import walkvec  # noqa: E402
+from walkvec import (Triple, build_graph, build_vocabulary, init_embeddings, train, TrainConfig,  # noqa: E402
+                     random_walks, bfs_walks, generate_pairs, assign_predicates, gen_barabasi)
+from walkvec import walks as ref_walks  # noqa: E402
+
+
+def rows_graph(rows):
+    vocab, edges = build_vocabulary([Triple(s, p, o) for s, p, o in rows])
+    return vocab, edges, build_graph(edges, len(vocab))
+
+
+def random_rows(rng, n_vertices, n_edges, n_predicates=3):
+    # same as the reference's tests/conftest.py:56-64 random_edge_rows
+    out = []
+    for _ in range(n_edges):
+        u = int(rng.integers(0, n_vertices))
+        v = int(rng.integers(0, n_vertices))
+        p = int(rng.integers(0, n_predicates))
+        out.append((f"v{u}", f"p{p}", f"v{v}"))
+    return out
+
+
+def philox_patch():
+    return mock.patch("numpy.random.default_rng", lambda ss: np.random.Generator(np.random.Philox(ss)))
+
+
+def seedseq():
+    ents = [[42, 0, 0], [42, 0, 7], [7, 0, 244140], [42, 1, 0], [42, 1, 2, 0], [123456789012, 0, 3], [0, 0, 0],
+            [2**40 + 5, 1, 1], [3, 0, 2**33 + 9]]
+    out = {"entropies": json.dumps(ents)}
+    for i, e in enumerate(ents):
+        ss = np.random.SeedSequence(e)
+        out[f"state4_{i}"] = ss.generate_state(4, np.uint64)
+        pcg = np.random.PCG64(np.random.SeedSequence(e))
+        out[f"pcg_{i}"] = pcg.random_raw(1100)[[0, 1, 2, 3, 999, 1000, 1099]]
+        ph = np.random.Philox(np.random.SeedSequence(e))
+        out[f"philox_{i}"] = ph.random_raw(1100)[[0, 1, 2, 3, 4, 5, 999, 1000, 1099]]
+    np.savez_compressed(OUT / "seedseq.npz", **out)
+
+
+def walks():
+    cases = {}
+    specs = [  # (graph seed, n_vertices, n_edges, depth, number, walk seed, root repeat, dup_free)
+        (11, 40, 200, 4, 1, 9, 410, False),      # > 2 shards incl. partial (reference worker test shape)
+        (12, 25, 100, 5, 3, 21, 1, False),
+        (0, 30, 120, 6, 4, 0, 1, False),
+        (3, 60, 90, 8, 7, 5, 1, False),          # sparse: many sinks / early termination
+        (4, 15, 40, 3, 500, 3, 1, True),         # duplicate_free
+        (5, 200, 700, 1, 2, 17, 1, False),
+        (6, 500, 1500, 8, 40, 123456789012, 1, False),  # 2-word seed, 20000 walks
+    ]
+    for ci, (gs, nv, ne, depth, number, seed, rep, dup) in enumerate(specs):
+        rng = np.random.default_rng(gs)
+        vocab, edges, g = rows_graph(random_rows(rng, nv, ne))
+        roots = np.repeat(vocab.entity_tokens(), rep)[: ref_walks.SHARD_SIZE * 2 + 17] if rep > 1 \
+            else vocab.entity_tokens()
+        c = random_walks(g, roots, walk_depth=depth, walk_number=number, rng_seed=seed, duplicate_free=dup)
+        with philox_patch():
+            cp = random_walks(g, roots, walk_depth=depth, walk_number=number, rng_seed=seed, duplicate_free=dup)
+        cases[f"c{ci}_edges"] = edges
+        cases[f"c{ci}_V"] = np.array(len(vocab))
+        cases[f"c{ci}_roots"] = roots
+        cases[f"c{ci}_params"] = np.array([depth, number, seed % (2**62), int(dup)], dtype=np.int64)
+        cases[f"c{ci}_seed"] = np.array(str(seed))
+        cases[f"c{ci}_pcg_tokens"] = c.tokens
+        cases[f"c{ci}_pcg_offsets"] = c.offsets
+        cases[f"c{ci}_philox_tokens"] = cp.tokens
+        cases[f"c{ci}_philox_offsets"] = cp.offsets
+        cases[f"c{ci}_row_offsets"] = g.row_offsets
+        cases[f"c{ci}_col_targets"] = g.col_targets
+        cases[f"c{ci}_col_predicates"] = g.col_predicates
+    cases["n_cases"] = np.array(len(specs))
+    np.savez_compressed(OUT / "walks.npz", **cases)
+
+
+def bfs():
+    cases = {}
+    rng = np.random.default_rng(77)
+    ci = 0
+    for trial in range(24):
+        n = int(rng.integers(4, 120))
+        ne = int(rng.integers(n, 4 * n))
+        if trial % 2 == 0:  # DAG like test_acceptance._random_dag_rows
+            order = rng.permutation(n)
+            rows = []
+            for _ in range(ne):
+                a, b = rng.integers(0, n, size=2)
+                if a == b:
+                    continue
+                u, v = (a, b) if order[a] < order[b] else (b, a)
+                rows.append((f"v{u}", f"p{int(rng.integers(0, 3))}", f"v{v}"))
+        else:
+            rows = random_rows(rng, n, ne)
+        if not rows:
+            continue
+        vocab, edges, g = rows_graph(rows)
+        depth = int(rng.integers(1, 7))
+        roots = vocab.entity_tokens()
+        corpus, table = bfs_walks(g, roots, depth)
+        cases[f"c{ci}_edges"] = edges
+        cases[f"c{ci}_V"] = np.array(len(vocab))
+        cases[f"c{ci}_depth"] = np.array(depth)
+        cases[f"c{ci}_roots"] = roots
+        cases[f"c{ci}_tokens"] = corpus.tokens
+        cases[f"c{ci}_offsets"] = corpus.offsets
+        cases[f"c{ci}_table"] = np.array(table.rows(), dtype=np.int64).reshape(-1, 3)
+        ci += 1
+    cases["n_cases"] = np.array(ci)
+    np.savez_compressed(OUT / "bfs.npz", **cases)
+
+
+def embeddings_and_train():
+    out = {}
+    inp = init_embeddings(37, 13, 5)
+    out["init_in"], out["init_out"] = inp.input_matrix, inp.output_matrix
+    # pairs with min_count filtering (windows close over gaps)
+    rng = np.random.default_rng(3)
+    seqs = [rng.integers(0, 12, size=int(rng.integers(1, 9))) for _ in range(60)]
+    lens = np.array([len(s) for s in seqs])
+    toks = np.concatenate(seqs)
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    corpus = walkvec.WalkCorpus(toks, offs, "random")
+    pairs, freq = generate_pairs(corpus, 3, 6, 12)
+    out["pairs_tokens"], out["pairs_offsets"], out["pairs"], out["pairs_freq"] = toks, offs, pairs, freq
+    # train cases on a small random-walk corpus
+    vocab, edges, g = rows_graph(random_rows(np.random.default_rng(21), 30, 150, 4))
+    c = random_walks(g, vocab.entity_tokens(), walk_depth=4, walk_number=6, rng_seed=4)
+    out["train_tokens"], out["train_offsets"], out["train_V"] = c.tokens, c.offsets, np.array(len(vocab))
+    cfgs = {
+        "sparse": dict(min_count=2, vector_size=12, epochs=2, window_size=3, negative_samples=4, learning_rate=0.02,
+                       batch_size=64),
+        "dense": dict(min_count=0, vector_size=8, epochs=1, window_size=2, negative_samples=2, learning_rate=0.01,
+                      batch_size=128, use_sparse=False),
+        "auto": dict(min_count=10, vector_size=16, epochs=1, window_size=5, negative_samples=5),
+        "multi": dict(min_count=0, vector_size=8, epochs=2, window_size=2, negative_samples=2, workers=2,
+                      reproducible=True, batch_size=16),
+        "multi3": dict(min_count=1, vector_size=6, epochs=1, window_size=3, negative_samples=1, workers=3,
+                       reproducible=True, batch_size=10),
+    }
+    for name, kw in cfgs.items():
+        model, losses = train(c, len(vocab), TrainConfig(**kw), 42)
+        out[f"{name}_in"], out[f"{name}_out"] = model.input_matrix, model.output_matrix
+        out[f"{name}_losses"] = np.array(losses)
+        out[f"{name}_touched_in"], out[f"{name}_touched_out"] = model.touched_input, model.touched_output
+        out[f"{name}_cfg"] = np.array(json.dumps(kw))
+    np.savez_compressed(OUT / "w2v.npz", **out)
+
+
+def two_clique():
+    rows = []
+    for base in ("x", "y"):
+        members = [f"{base}{i}" for i in range(5)]
+        rows += [(u, "p", v) for u in members for v in members if u != v]
+    rows.append(("x0", "p", "y0"))
+    vocab, edges, g = rows_graph(rows)
+    res = []
+    for seed in range(10):
+        corpus = random_walks(g, vocab.entity_tokens(), walk_depth=4, walk_number=25, rng_seed=42 + seed)
+        cfg = TrainConfig(min_count=1, vector_size=16, epochs=10, learning_rate=0.01, window_size=5,
+                          negative_samples=5)
+        model, losses = train(corpus, len(vocab), cfg, 42 + seed)
+        v = model.input_matrix
+        x = [vocab.token_of[f"x{i}"] for i in range(5)]
+        y = [vocab.token_of[f"y{i}"] for i in range(5)]
+
+        def cos(a, b):
+            return float(np.dot(v[a], v[b]) / (np.linalg.norm(v[a]) * np.linalg.norm(v[b])))
+
+        intra = [cos(a, b) for grp in (x, y) for a in grp for b in grp if a < b]
+        inter = [cos(a, b) for a in x for b in y]
+        res.append(dict(seed=42 + seed, margin=float(np.mean(intra) - np.mean(inter)), loss0=losses[0],
+                        loss_last=losses[-1]))
+    (OUT / "two_clique.json").write_text(json.dumps(dict(edges=edges.tolist(), V=len(vocab),
+                                                         x=[vocab.token_of[f"x{i}"] for i in range(5)],
+                                                         y=[vocab.token_of[f"y{i}"] for i in range(5)],
+                                                         roots=vocab.entity_tokens().tolist(), runs=res), indent=1))
+
+
+def vocab_encoding():
+    e2 = gen_barabasi(300, 3, seed=7)
+    triples = assign_predicates(e2, 5, seed=7)
+    vocab, edges = build_vocabulary(triples)
+    picks = np.array([int(t.predicate[1:]) for t in triples])
+    np.savez_compressed(OUT / "vocab.npz", raw=e2, picks=picks, edges=edges, entity_tokens=vocab.entity_tokens(),
+                        V=np.array(len(vocab)))
+
+
+if __name__ == "__main__":
+    seedseq()
+    walks()
+    bfs()
+    embeddings_and_train()
+    two_clique()
+    vocab_encoding()
+    for p in sorted(OUT.glob("*.np*")) + sorted(OUT.glob("*.json")):
+        print(p.name, p.stat().st_size)

@@ -1,0 +1,177 @@
+"""GPU parity: CSR, random walks (PCG64 / Philox streams), BFS, projections vs the reference fixtures + oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import walks as ow
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wv():
+    import paper_2508_01073_b200 as wv
+
+    return wv
+
+
+def _case(g, i):
+    p = g[f"c{i}_params"]
+    return (g[f"c{i}_edges"], int(g[f"c{i}_V"]), g[f"c{i}_roots"], int(p[0]), int(p[1]), int(str(g[f"c{i}_seed"])),
+            bool(p[3]))
+
+
+def test_csr_matches_reference(golden, wv):
+    g = golden("walks.npz")
+    for i in range(int(g["n_cases"])):
+        edges, V, *_ = _case(g, i)
+        graph = wv.build_graph(edges, V)
+        assert np.array_equal(graph.row_offsets, g[f"c{i}_row_offsets"])
+        assert np.array_equal(graph.col_targets, g[f"c{i}_col_targets"])
+        assert np.array_equal(graph.col_predicates, g[f"c{i}_col_predicates"])
+
+
+def test_csr_stable_large(wv):
+    rng = np.random.default_rng(5)
+    E, V = 300_000, 50_000
+    edges = np.stack([rng.integers(0, 50, E), rng.integers(0, V, E), rng.integers(0, V, E)], 1)  # heavy rows
+    graph = wv.build_graph(edges, V)
+    off, tgt, prd = ow.csr(edges, V)
+    assert np.array_equal(graph.row_offsets, off)
+    assert np.array_equal(graph.col_targets, tgt)
+    assert np.array_equal(graph.col_predicates, prd)
+
+
+def test_csr_errors(wv):
+    with pytest.raises(ValueError):
+        wv.build_graph(np.array([[0, 1, 5]]), 3)
+    with pytest.raises(ValueError):
+        wv.build_graph(np.zeros((2, 2), dtype=np.int64), 3)
+
+
+@pytest.mark.parametrize("rng", ["pcg64", "philox"])
+def test_random_walks_bit_exact_vs_reference(golden, wv, rng):
+    g = golden("walks.npz")
+    tag = "pcg" if rng == "pcg64" else "philox"
+    for i in range(int(g["n_cases"])):
+        edges, V, roots, depth, number, seed, dup = _case(g, i)
+        graph = wv.build_graph(edges, V)
+        c = wv.random_walks(graph, roots, walk_depth=depth, walk_number=number, rng_seed=seed, duplicate_free=dup,
+                            rng=rng)
+        assert np.array_equal(c.tokens, g[f"c{i}_{tag}_tokens"]), (rng, i)
+        assert np.array_equal(c.offsets, g[f"c{i}_{tag}_offsets"]), (rng, i)
+
+
+def test_walk_slices_union_is_full_corpus(golden, wv):
+    """Multi-GPU contract: disjoint work ranges concatenate to the single-launch corpus."""
+    import torch
+    from paper_2508_01073_b200 import walks as W
+    from paper_2508_01073_b200.dist import walk_work_range
+
+    g = golden("walks.npz")
+    edges, V, roots, depth, number, seed, _ = _case(g, 6)
+    graph = wv.build_graph(edges, V)
+    d_roots = torch.from_numpy(roots).cuda()
+    full, flen, width = W.random_walks_fixed(graph, d_roots, depth, number, seed)
+    parts, plens = [], []
+    for r in range(3):
+        b, e = walk_work_range(len(roots), number, r, 3)
+        c, l, _ = W.random_walks_fixed(graph, d_roots, depth, number, seed, work_begin=b, work_count=e - b)
+        parts.append(c[: (e - b) * width])
+        plens.append(l[: e - b])
+    assert torch.equal(torch.cat(parts), full[: len(roots) * number * width])
+    assert torch.equal(torch.cat(plens), flen[: len(roots) * number])
+
+
+def test_random_walks_large_vs_oracle_shards(wv):
+    """A 1M-walk run: sampled shards bit-exact against the oracle, plus global validity."""
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("barabasi", 20_000, m=5, predicates=20, seed=7)
+    graph = wv.build_graph(edges, V)
+    c = wv.random_walks(graph, ents, walk_depth=6, walk_number=50, rng_seed=42)
+    off, tgt, prd = ow.csr(edges, V)
+    n_sh = -(-len(ents) * 50 // ow.SHARD)
+    for s in (0, 7, n_sh - 1):
+        tok, offs = ow.random_walks(off, tgt, prd, ents, 6, 50, 42, "pcg64", shards=[s])
+        w0 = s * ow.SHARD
+        lo, hi = c.offsets[w0], c.offsets[min(w0 + ow.SHARD, len(c))]
+        assert np.array_equal(c.tokens[lo:hi], tok)
+    # every hop is an edge
+    t = c.tokens
+    starts = c.offsets[:-1]
+    lens = np.diff(c.offsets)
+    assert (lens % 2 == 1).all() and lens.max() <= 13
+    key = set(map(tuple, edges.tolist()))
+    sample = np.random.default_rng(0).choice(len(c), 2000, replace=False)
+    for w in sample:
+        seq = t[starts[w]: starts[w] + lens[w]]
+        for j in range(0, len(seq) - 2, 2):
+            assert (seq[j], seq[j + 1], seq[j + 2]) in key
+
+
+def test_hop_distribution_chi_square(wv):
+    """Uniform choice among out-edges: chi-square per vertex over many walks (north_star fallback check)."""
+    from scipy.stats import chisquare
+
+    rng = np.random.default_rng(9)
+    edges = np.stack([np.zeros(7, dtype=np.int64), np.arange(7) + 8, np.arange(1, 8)], 1)
+    graph = wv.build_graph(edges, 15)
+    c = wv.random_walks(graph, [0], walk_depth=1, walk_number=70_000, rng_seed=3, rng="philox")
+    first = c.tokens.reshape(-1, 3)[:, 2]
+    counts = np.bincount(first, minlength=8)[1:]
+    assert chisquare(counts).pvalue > 1e-3
+
+
+def test_walk_edge_cases(wv):
+    edges = np.array([[0, 3, 1], [1, 4, 2]])  # a -p-> b -q-> c
+    graph = wv.build_graph(edges, 5)
+    assert wv.random_walks(graph, [0], walk_depth=4).tokens.tolist() == [0, 3, 1, 4, 2]
+    assert wv.random_walks(graph, [2], walk_depth=8, rng_seed=1).tokens.tolist() == [2]
+    c = wv.random_walks(graph, [0], walk_depth=4, walk_number=500, rng_seed=3, duplicate_free=True)
+    assert len(c) == 1
+    with pytest.raises(ValueError):
+        wv.random_walks(graph, [0], walk_depth=0)
+    with pytest.raises(ValueError):
+        wv.random_walks(graph, [], walk_depth=2)
+    with pytest.raises(ValueError):
+        wv.random_walks(graph, [99], walk_depth=2)
+
+
+@pytest.mark.parametrize("projection", ["entity", "property"])
+def test_projection_matches_oracle(golden, wv, projection):
+    g = golden("walks.npz")
+    edges, V, roots, depth, number, seed, _ = _case(g, 2)
+    c = wv.random_walks(wv.build_graph(edges, V), roots, walk_depth=depth, walk_number=number, rng_seed=seed)
+    p = wv.project_corpus(c, projection)
+    tok, offs = ow.project(g["c2_pcg_tokens"], g["c2_pcg_offsets"], projection)
+    assert np.array_equal(p.tokens, tok) and np.array_equal(p.offsets, offs)
+    with pytest.raises(ValueError):
+        wv.project_corpus(p, "entity")
+
+
+def test_bfs_bit_exact_vs_reference(golden, wv):
+    g = golden("bfs.npz")
+    for i in range(int(g["n_cases"])):
+        graph = wv.build_graph(g[f"c{i}_edges"], int(g[f"c{i}_V"]))
+        corpus, table = wv.bfs_walks(graph, g[f"c{i}_roots"], int(g[f"c{i}_depth"]))
+        assert np.array_equal(corpus.tokens, g[f"c{i}_tokens"]), i
+        assert np.array_equal(corpus.offsets, g[f"c{i}_offsets"]), i
+        assert np.array_equal(np.array(table.rows(), dtype=np.int64).reshape(-1, 3), g[f"c{i}_table"]), i
+
+
+def test_bfs_cap_is_prefix_and_large_trees(wv):
+    """Trees beyond the shared-memory tier (fallback) and the max-walks cap as a per-root prefix."""
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("barabasi", 30_000, m=10, predicates=20, seed=7)
+    graph = wv.build_graph(edges, V)
+    off, tgt, prd = ow.csr(edges, V)
+    rs = np.random.default_rng(1).choice(ents, 12, replace=False)
+    roots = np.concatenate([rs, ents[-3:]])  # newest vertices: biggest trees
+    corpus, _ = wv.bfs_walks(graph, roots, 4)
+    tok, offs, _ = ow.bfs_walks(off, tgt, prd, roots, 4)
+    assert np.array_equal(corpus.tokens, tok) and np.array_equal(corpus.offsets, offs)
+    capped, _ = wv.bfs_walks(graph, roots, 4, max_walks_per_root=250)
+    tok, offs, _ = ow.bfs_walks(off, tgt, prd, roots, 4, cap=250)
+    assert np.array_equal(capped.tokens, tok) and np.array_equal(capped.offsets, offs)
