@@ -47,6 +47,16 @@ int wv_abi_version(void);
 /* sizeof of the ABI structs (0 WvSgnsDevState, 1 WvSgnsModel, 2 WvSgnsBatch) for binding checks */
 int64_t wv_struct_size(int which);
 int wv_stream_sync(void* stream);
+/* kernels this library has enqueued so far (host-side count; a CUDA-graph
+ * capture counts its launches once, replays are not seen here) */
+int64_t wv_launch_count(void);
+/* n CUDA events for kernel timing; records made while `stream` is being
+ * captured into a CUDA graph become external event-record nodes, so a
+ * replayed graph still timestamps its phases (profiling / bench roofline). */
+void* wv_timer_create(int n);
+int wv_timer_record(void* timer, int i, void* stream);
+int wv_timer_elapsed(void* timer, int i, int j, float* ms);
+int wv_timer_destroy(void* timer);
 
 /* numpy SeedSequence(prefix + [index]).generate_state(n64, uint64) on the host.
  * prefix = little-endian u32 words of the leading entropy integers. */
@@ -214,6 +224,28 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
 int wv_replica_delta(const void* params, const void* snapshot, int64_t n, int precision, void* delta, void* stream);
 int wv_replica_apply(void* params, void* snapshot, const void* delta_sum, const float* touch_count, int64_t rows,
                      int vector_size, int precision, void* stream);
+
+/* ------------------------------------------------------------ synthetic --
+ * Measurement inputs (BASELINE.json configs).  gen_barabasi restates
+ * benchgen.gen_barabasi (benchgen.py:78-109): vertex v >= 1 adds min(m, v)
+ * distinct edges v -> t, t drawn from the degree+1 attachment bag.  Same
+ * process, counter-based draws (not numpy's stream).  src/dst int64 sized
+ * wv_barabasi_edge_count(n, m), ordered by source then draw slot like the
+ * reference.  Synchronises `stream` (a few convergence rounds). */
+int64_t wv_barabasi_edge_count(int64_t n, int m);
+int64_t wv_barabasi_workspace_bytes(int64_t n, int m);
+int wv_gen_barabasi(int64_t n, int m, uint64_t seed, int64_t* src, int64_t* dst, void* ws, int64_t ws_bytes,
+                    void* stream);
+/* First-occurrence token encoding of integer triples (ingest.build_vocabulary,
+ * ingest.py:368-396, over benchgen.assign_predicates' "v{u}"/"P{k}" triples,
+ * benchgen.py:152-161).  Keys: entity u -> u, predicate k -> n_entities + k.
+ * edges_out (E,3) int64 tokens (may be NULL); token_of_key[n_keys] (-1 when
+ * absent); key_of_token[n_keys] (-1 past the vocabulary; may be NULL);
+ * *vocab_size is a device int64. */
+int64_t wv_encode_workspace_bytes(int64_t E, int64_t n_keys);
+int wv_encode_triples(const int64_t* src, const int64_t* preds, const int64_t* dst, int64_t E, int64_t n_entities,
+                      int64_t n_predicates, int64_t* edges_out, int64_t* token_of_key, int64_t* key_of_token,
+                      int64_t* vocab_size, void* ws, int64_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ from .w2v import (
     CBOW,
     SKIPGRAM,
     EmbeddingModel,
+    SkipGramSession,
     TrainConfig,
     TrainingDiverged,
     estimate_per_sample_bytes,
@@ -52,7 +53,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BFS", "CBOW", "ENTITY", "FULL", "PAD", "PROPERTY", "RANDOM", "SHARD_SIZE", "SKIPGRAM",
     "BackendUnavailable", "EmbeddingModel", "EmbeddingTable", "Graph", "PathTable", "PipelineConfig",
-    "PipelineError", "TrainConfig", "TrainingDiverged", "Vocabulary", "Walk", "WalkCorpus",
+    "PipelineError", "SkipGramSession", "TrainConfig", "TrainingDiverged", "Vocabulary", "Walk", "WalkCorpus",
     "bfs_walks", "build_graph", "build_vocabulary", "encode_integer_triples", "estimate_per_sample_bytes",
     "extract_walks", "fit_transform", "generate_pairs", "init_embeddings", "install", "project_corpus",
     "project_entity", "project_property", "random_walks", "resolve_memory_budget", "suggest_batch_size",

@@ -113,6 +113,11 @@ SIGNATURES = {
     "wv_abi_version": (I32, []),
     "wv_struct_size": (I64, [I32]),
     "wv_stream_sync": (I32, [P]),
+    "wv_launch_count": (I64, []),
+    "wv_timer_create": (P, [I32]),
+    "wv_timer_record": (I32, [P, I32, P]),
+    "wv_timer_elapsed": (I32, [P, I32, I32, P]),
+    "wv_timer_destroy": (I32, [P]),
     "wv_seedseq_generate": (I32, [P, I32, U64, I32, P]),
     "wv_stream_u64": (I32, [P, I32, U64, I32, U64, P]),
     "wv_csr_workspace_bytes": (I64, [I64, I64]),
@@ -144,6 +149,11 @@ SIGNATURES = {
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
     "wv_replica_delta": (I32, [P, P, I64, I32, P, P]),
     "wv_replica_apply": (I32, [P, P, P, P, I64, I32, I32, P]),
+    "wv_barabasi_edge_count": (I64, [I64, I32]),
+    "wv_barabasi_workspace_bytes": (I64, [I64, I32]),
+    "wv_gen_barabasi": (I32, [I64, I32, U64, P, P, P, I64, P]),
+    "wv_encode_workspace_bytes": (I64, [I64, I64]),
+    "wv_encode_triples": (I32, [P, P, P, I64, I64, I64, P, P, P, P, P, I64, P]),
 }
 
 _lock = threading.Lock()
@@ -183,6 +193,43 @@ def call(name: str, *args):
             raise ValueError(msg)
         raise WvError(f"{name}: {msg}")
     return rc
+
+
+_graph_replayed_launches = 0
+
+
+def note_graph_replay(launches: int):
+    """Count the kernels a CUDA-graph replay re-issues (the C side sees only the capture)."""
+    global _graph_replayed_launches
+    _graph_replayed_launches += int(launches)
+
+
+def launch_count() -> int:
+    """Kernels of this library enqueued so far: direct launches + graph replays."""
+    return int(load().wv_launch_count()) + _graph_replayed_launches
+
+
+class DeviceTimer:
+    """``n`` CUDA events that also timestamp inside captured CUDA graphs (external records)."""
+
+    def __init__(self, n: int):
+        self.n = int(n)
+        self.h = load().wv_timer_create(self.n)
+        if not self.h:
+            raise WvError(load().wv_last_error().decode())
+
+    def record(self, i: int, stream=None):
+        call("wv_timer_record", self.h, int(i), stream_ptr(stream))
+
+    def elapsed(self, i: int, j: int) -> float:
+        ms = C.c_float(0.0)
+        call("wv_timer_elapsed", self.h, int(i), int(j), C.byref(ms))
+        return float(ms.value)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.wv_timer_destroy(self.h)
+            self.h = None
 
 
 def query(name: str, *args) -> int:

@@ -1,12 +1,17 @@
 // C-ABI plumbing: thread-local error text, version, device queries.
 #include <cstdarg>
 #include <cstdio>
+#include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "../../include/walkvec_b200.h"
 
 namespace wv {
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -21,6 +26,8 @@ extern "C" {
 const char* wv_last_error(void) { return wv::g_err; }
 
 int wv_abi_version(void) { return WV_ABI_VERSION; }
+
+int64_t wv_launch_count(void) { return (int64_t)wv::g_launches.load(std::memory_order_relaxed); }
 
 int64_t wv_struct_size(int which) {
   switch (which) {
@@ -72,6 +79,59 @@ int wv_stream_u64(const uint32_t* entropy_prefix, int n_prefix, uint64_t index, 
   }
   wv::set_error("unknown rng kind %d", kind);
   return -1;
+}
+
+// ---- device timers usable inside CUDA-graph capture (external event records)
+struct WvTimer {
+  int n;
+  cudaEvent_t ev[1];
+};
+
+void* wv_timer_create(int n) {
+  if (n < 1) {
+    wv::set_error("timer needs >= 1 event");
+    return nullptr;
+  }
+  WvTimer* t = (WvTimer*)malloc(sizeof(WvTimer) + sizeof(cudaEvent_t) * (n - 1));
+  if (!t) return nullptr;
+  t->n = n;
+  for (int i = 0; i < n; ++i) {
+    if (cudaEventCreate(&t->ev[i]) != cudaSuccess) {
+      for (int j = 0; j < i; ++j) cudaEventDestroy(t->ev[j]);
+      free(t);
+      wv::set_error("cudaEventCreate failed");
+      return nullptr;
+    }
+  }
+  return t;
+}
+
+int wv_timer_record(void* timer, int i, void* stream) {
+  WvTimer* t = (WvTimer*)timer;
+  WV_CHECK_ARG(t && i >= 0 && i < t->n, "bad timer slot");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  WV_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    WV_CUDA(cudaEventRecordWithFlags(t->ev[i], st, cudaEventRecordExternal));
+  else
+    WV_CUDA(cudaEventRecord(t->ev[i], st));
+  return 0;
+}
+
+int wv_timer_elapsed(void* timer, int i, int j, float* ms) {
+  WvTimer* t = (WvTimer*)timer;
+  WV_CHECK_ARG(t && i >= 0 && i < t->n && j >= 0 && j < t->n, "bad timer slot");
+  WV_CUDA(cudaEventElapsedTime(ms, t->ev[i], t->ev[j]));
+  return 0;
+}
+
+int wv_timer_destroy(void* timer) {
+  WvTimer* t = (WvTimer*)timer;
+  if (!t) return 0;
+  for (int i = 0; i < t->n; ++i) cudaEventDestroy(t->ev[i]);
+  free(t);
+  return 0;
 }
 
 }  // extern "C"

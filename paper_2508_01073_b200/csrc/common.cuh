@@ -230,6 +230,7 @@ WV_HD uint64_t splitmix64(uint64_t x) {
 // ------------------------------------------------------ error handling ----
 namespace wv {
 void set_error(const char* fmt, ...);
+void note_launches(int n);
 }
 
 #define WV_CHECK_ARG(cond, ...)          \
@@ -251,6 +252,7 @@ void set_error(const char* fmt, ...);
 
 #define WV_LAUNCH_CHECK()                                                          \
   do {                                                                             \
+    ::wv::note_launches(1);                                                        \
     cudaError_t _e = cudaGetLastError();                                           \
     if (_e != cudaSuccess) {                                                       \
       ::wv::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \

@@ -12,6 +12,10 @@
 
 namespace wv {
 
+// host-side count of kernels this library has enqueued (abi.cu); graph
+// captures count once per captured launch
+void note_launches(int n);
+
 constexpr int kScanThreads = 512;
 constexpr int kScanIpt = 8;
 constexpr int64_t kScanTile = (int64_t)kScanThreads * kScanIpt;
@@ -113,6 +117,7 @@ inline cudaError_t excl_scan(const Tin* in, int64_t n, T* out, T* total, T* ws, 
     return cudaSuccess;
   }
   int64_t tiles = scan_tiles(n);
+  note_launches(3);
   scan_tile_reduce<Tin, T><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, n, ws);
   scan_carry<T><<<1, kScanThreads, 0, st>>>(ws, tiles, total);
   scan_tile_apply<Tin, T><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, n, ws, out);
@@ -230,6 +235,7 @@ inline cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, i
   uint32_t *ka = keys, *va = vals, *kb = k2, *vb = v2;
   for (int pass = 0; pass < p.passes; ++pass) {
     int shift = pass * 8;
+    note_launches(2);
     if (p.ipt == 16) {
       radix_hist<16><<<(unsigned)p.tiles, kRadixThreads, 0, st>>>(ka, n, shift, hist, p.tiles);
     } else {

@@ -124,3 +124,73 @@ def synthetic_kg(model: str, n: int, m: int = 10, p: float = 0.001, predicates: 
         raise ValueError(f"unknown model {model!r}")
     picks = predicate_picks(len(e2), predicates, seed)
     return encode_integer_triples(e2[:, 0], picks, e2[:, 1], n)
+
+
+# ------------------------------------------------------------------ device --
+def device_barabasi_edges(n: int, m: int, seed: int = 7, device=None):
+    """(src, dst) int64 device tensors of a preferential-attachment graph (csrc/synth.cu)."""
+    from . import _lib
+
+    torch = _lib.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    E = _lib.query("wv_barabasi_edge_count", n, m)
+    src = torch.empty(E, dtype=torch.int64, device=dev)
+    dst = torch.empty(E, dtype=torch.int64, device=dev)
+    ws = torch.empty(_lib.query("wv_barabasi_workspace_bytes", n, m), dtype=torch.uint8, device=dev)
+    _lib.call("wv_gen_barabasi", n, m, int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(src), _lib.ptr(dst), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    return src, dst
+
+
+def device_encode(src, preds, dst, n_entities: int, n_predicates: int):
+    """First-occurrence encoding on the device -> (edges (E,3), vocab_size, entity_tokens, predicate_tokens).
+
+    Token arrays are sorted int64 device tensors (ingest.py:282-284).
+    """
+    from . import _lib
+
+    torch = _lib.require_cuda()
+    dev = src.device
+    E = int(src.numel())
+    n_keys = int(n_entities) + int(n_predicates)
+    edges = torch.empty((max(E, 1), 3), dtype=torch.int64, device=dev)
+    tok_of_key = torch.empty(n_keys, dtype=torch.int64, device=dev)
+    key_of_tok = torch.empty(n_keys, dtype=torch.int64, device=dev)
+    vocab = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(_lib.query("wv_encode_workspace_bytes", E, n_keys), dtype=torch.uint8, device=dev)
+    _lib.call("wv_encode_triples", _lib.ptr(src), _lib.ptr(preds), _lib.ptr(dst), E, int(n_entities),
+              int(n_predicates), _lib.ptr(edges), _lib.ptr(tok_of_key), _lib.ptr(key_of_tok), _lib.ptr(vocab),
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    V = int(vocab.item())
+    kot = key_of_tok[:V]
+    ent = torch.nonzero(kot < int(n_entities)).flatten()
+    prd = torch.nonzero(kot >= int(n_entities)).flatten()
+    return edges[:E], V, ent, prd
+
+
+def device_synthetic_kg(model: str, n: int, m: int = 10, predicates: int = 10, seed: int = 7, p: float = 0.001,
+                        device=None):
+    """synthetic_kg with the edge generator and the token encoding on the device.
+
+    Predicates are drawn from the reference's own stream (assign_predicates,
+    SeedSequence([seed, 3]).integers) on the host.  Returns
+    (edges (E,3) device int64, vocab_size, entity_tokens, predicate_tokens).
+    """
+    from . import _lib
+
+    torch = _lib.require_cuda()
+    if model == "barabasi":
+        src, dst = device_barabasi_edges(n, m, seed, device)
+    elif model == "erdos_renyi":
+        e2 = erdos_renyi_edges(n, p, seed)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        src = torch.from_numpy(np.ascontiguousarray(e2[:, 0])).to(dev)
+        dst = torch.from_numpy(np.ascontiguousarray(e2[:, 1])).to(dev)
+    else:
+        raise ValueError(f"unknown model {model!r}")
+    picks = torch.from_numpy(predicate_picks(int(src.numel()), predicates, seed)).to(src.device)
+    return device_encode(src, picks, dst, n, predicates)

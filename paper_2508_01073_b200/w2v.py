@@ -366,10 +366,11 @@ class _Replica:
                                          trainer.batch_size, params.precision), dtype=torch.uint8,
                               device=trainer.dev)
         self.graphs = {}
-        self.graph_events = {}  # key -> [G][4] CUDA events of the last replay (profiling)
+        self.graph_events = {}  # key -> DeviceTimer of 4 events per batch, last replay (profiling)
+        self.graph_launches = {}  # key -> kernels per replay
 
     def launch(self, rows: int, events=None):
-        """One batch; ``events`` = 4 CUDA events recorded around the three phases."""
+        """One batch; ``events`` = (DeviceTimer, first slot): 4 stamps around the three phases."""
         t = self.t
         bs = t.batch_struct
         bs.batch_rows = int(rows)
@@ -377,11 +378,12 @@ class _Replica:
             _lib.call("wv_sgns_batch", C.byref(self.p.struct), C.byref(bs), _lib.ptr(self.ws), self.ws.numel(),
                       _lib.stream_ptr())
             return
-        events[0].record()
+        timer, base = events
+        timer.record(base)
         for i, ph in enumerate((_lib.PHASE_PAIRS, _lib.PHASE_GROUP, _lib.PHASE_UPDATE)):
             _lib.call("wv_sgns_batch_phases", C.byref(self.p.struct), C.byref(bs), _lib.ptr(self.ws),
                       self.ws.numel(), ph, _lib.stream_ptr())
-            events[i + 1].record()
+            timer.record(base + i + 1)
 
     def run(self, count: int, rows: int):
         """``count`` consecutive batches of ``rows`` pairs, CUDA-graph replayed."""
@@ -399,15 +401,19 @@ class _Replica:
             g = torch.cuda.CUDAGraph()
             evs = None
             if self.t.profile:
-                evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(key[1])]
+                evs = _lib.DeviceTimer(4 * key[1])
+            before = _lib.launch_count()
             with torch.cuda.graph(g):
                 for i in range(key[1]):
-                    self.launch(rows, None if evs is None else evs[i])
+                    self.launch(rows, None if evs is None else (evs, 4 * i))
             self.graphs[key] = g
             self.graph_events[key] = evs
+            self.graph_launches[key] = _lib.launch_count() - before
+            _lib.note_graph_replay(-self.graph_launches[key])  # the capture itself runs nothing
         g = self.graphs[key]
         for _ in range(reps):
             g.replay()
+        _lib.note_graph_replay(reps * self.graph_launches[key])
         for _ in range(rem):
             self.launch(rows)
 
@@ -610,6 +616,121 @@ class _Trainer:
         batch_bytes = rows * c.vector_size * es * 2 + min(rows, 2 * self.V) * c.vector_size * es * 8
         est_ms = max(batch_bytes / 3.0e12 * 1e3, 0.02)
         return max(1, min(int(round(c.sync_interval_ms / est_ms)), 1 << 14))
+
+
+class SkipGramSession:
+    """Persistent SGNS state trained over a sequence of corpora (streaming ``train``).
+
+    One parameter store and its RowAdam state stay resident in HBM while
+    corpora arrive -- e.g. the walks of successive root blocks of a graph too
+    large to walk in one piece.  Each ``fit`` runs ``epochs`` passes over that
+    corpus's pairs with train()'s batch rule, kernels and numerics
+    (w2v.py:547-576).  Negatives are drawn uniformly over the whole
+    vocabulary: min_count filtering needs global frequencies, which one block
+    does not have (with walk_number >= min_count every root token passes
+    anyway).  Epoch streams (Feistel permutation key, Philox
+    negatives) advance with a session-wide epoch counter.
+    """
+
+    def __init__(self, vocab_size: int, config: TrainConfig, rng_seed: int, *, precision: str = "fp32",
+                 graph_batches: int = 64, device=None, on_event=None):
+        if config.model != SKIPGRAM:
+            raise NotImplementedError("the B200 backend implements model='skipgram'")
+        if precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
+        torch = _lib.require_cuda()
+        self.torch = torch
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.config = config
+        self.V = int(vocab_size)
+        self.seed = int(rng_seed)
+        self.precision = precision
+        self.graph_batches = int(graph_batches)
+        self.events = on_event or (lambda kind, **info: None)
+        self.params = _Params(torch, self.dev, self.V, config.vector_size, self.seed, precision, config.use_sparse,
+                              config.learning_rate)
+        self.epochs_done = 0
+        self.pairs_done = 0
+        self.batches_done = 0
+        self.last_batch_size = 0
+        self.last_replica = None
+        self.exchange = None
+
+    def attach_exchange(self, exchange):
+        """Join a data-parallel group: sync() then averages per-row deltas across ranks
+        (_merge_bundles semantics, w2v.py:642-659) every time it is called."""
+        torch, p = self.torch, self.params
+        self.exchange = exchange
+        self._round_in = torch.zeros(self.V, dtype=torch.uint8, device=self.dev)
+        self._round_out = torch.zeros(self.V, dtype=torch.uint8, device=self.dev)
+        p.struct.touched_in = _lib.ptr(self._round_in)
+        p.struct.touched_out = _lib.ptr(self._round_out)
+        self._snap_in = p.inp.clone()
+        self._snap_out = p.out.clone()
+        self._delta_in = torch.empty_like(p.inp)
+        self._delta_out = torch.empty_like(p.out)
+        self._cnt_in = torch.empty(self.V, dtype=torch.float32, device=self.dev)
+        self._cnt_out = torch.empty(self.V, dtype=torch.float32, device=self.dev)
+
+    def sync(self):
+        """One replica-averaging round over the attached exchange (one all-reduce of deltas + counts)."""
+        if self.exchange is None:
+            return
+        p, st = self.params, _lib.stream_ptr()
+        n_el = self.V * self.config.vector_size
+        _lib.call("wv_replica_delta", _lib.ptr(p.inp), _lib.ptr(self._snap_in), n_el, p.precision,
+                  _lib.ptr(self._delta_in), st)
+        _lib.call("wv_replica_delta", _lib.ptr(p.out), _lib.ptr(self._snap_out), n_el, p.precision,
+                  _lib.ptr(self._delta_out), st)
+        self._cnt_in.copy_(self._round_in)
+        self._cnt_out.copy_(self._round_out)
+        p.touched_in |= self._round_in
+        p.touched_out |= self._round_out
+        self._round_in.zero_()
+        self._round_out.zero_()
+        self.exchange.all_reduce_(self._delta_in, self._delta_out, self._cnt_in, self._cnt_out)
+        _lib.call("wv_replica_apply", _lib.ptr(p.inp), _lib.ptr(self._snap_in), _lib.ptr(self._delta_in),
+                  _lib.ptr(self._cnt_in), self.V, self.config.vector_size, p.precision, st)
+        _lib.call("wv_replica_apply", _lib.ptr(p.out), _lib.ptr(self._snap_out), _lib.ptr(self._delta_out),
+                  _lib.ptr(self._cnt_out), self.V, self.config.vector_size, p.precision, st)
+
+    def fit(self, corpus, epochs: int = 1, *, profile: bool = False) -> list[float]:
+        """Train ``epochs`` passes over ``corpus``; returns the per-epoch mean losses."""
+        from dataclasses import replace
+
+        cfg = replace(self.config, min_count=0, epochs=int(epochs), workers=1)
+        tr = _Trainer(corpus, self.V, cfg, self.seed, self.events, self.precision, "device", self.graph_batches,
+                      device=self.dev)
+        tr.profile = profile
+        rep = _Replica(tr, 0, self.params)
+        self.last_replica = rep
+        B, N = tr.batch_size, tr.N
+        full, rem = divmod(N, B)
+        p = self.params
+        losses = []
+        for _ in range(int(epochs)):
+            _lib.call("wv_sgns_epoch_begin", _lib.ptr(p.state), self.epochs_done, 0, _lib.stream_ptr())
+            rep.run(full, B)
+            if rem:
+                rep.launch(rem)
+            st = p.read_state()
+            if st.diverged_batch >= 0:
+                raise TrainingDiverged(int(st.diverged_epoch), int(st.diverged_batch))
+            losses.append(st.epoch_loss_sum / st.epoch_count)
+            self.epochs_done += 1
+            self.pairs_done += N
+            self.batches_done += full + (1 if rem else 0)
+        self.last_batch_size = B
+        self.last_pairs = N
+        return losses
+
+    def rows_updated(self) -> int:
+        """Cumulative unique (row, matrix) Adam updates (telemetry for the roofline)."""
+        return int(self.params.read_state().rows_updated)
+
+    @property
+    def model(self) -> EmbeddingModel:
+        return EmbeddingModel(self.params, self.config.vector_size, np.ones(self.V, dtype=bool))
 
 
 def train(corpus, vocab_size: int, config: TrainConfig, rng_seed: int, on_event=None, *, precision: str = "fp32",
