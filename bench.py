@@ -45,6 +45,10 @@ METRIC = "walk hops/s + SGNS pairs/s at 1/2/4/8 B200; end-to-end RDF2vec sec vs 
 N_ENT, M_BA, N_PRED, GEN_SEED = 1_000_000, 10, 200, 7
 DEPTH, WALKS, DIM, WINDOW, NEG, LR, SEED = 8, 100, 200, 5, 5, 0.01, 42
 BUDGET = 1 << 30
+# per-batch device timestamps (w2v.STAMPS_PER_BATCH): start, decode end, gather end, join, owner end,
+# sort start, sort end
+STAMPS = 7
+PHASES = {"decode": (0, 1), "gather": (1, 2), "sort": (5, 6), "owner": (3, 4), "batch": (0, 4)}
 
 
 def workload(roots_per_step: int) -> dict:
@@ -297,10 +301,9 @@ def run_ours(args, rank, world, local):
         b = (step * world + rank) % n_blocks
         return b * R, min((b + 1) * R, n_roots)
 
-    stats = {"walk_ms": [], "hops": 0, "walks": 0, "pairs": 0, "batches": 0, "sgns_ms": [],
-             "phase_ms": [[], [], []], "phase_batches": 0}
+    stats = {"walk_ms": [], "hops": 0, "walks": 0, "pairs": 0, "batches": 0, "sgns_ms": [], "phase_ms": {}}
 
-    def one_step(step, timed):
+    def one_step(step, timed, profile=False):
         rb, re_ = block_range(step)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
@@ -309,7 +312,7 @@ def run_ours(args, rank, world, local):
         e1.record(stream)
         n_w = (re_ - rb) * WALKS
         wc = wmod._compact(torch, dev, corpus, lengths, n_w, width, wmod.RANDOM)
-        sess.fit(wc, 1, profile=timed)
+        sess.fit(wc, 1, profile=profile)
         sess.sync()
         e2.record(stream)
         if timed:
@@ -320,13 +323,17 @@ def run_ours(args, rank, world, local):
             stats["walks"] += n_w
             stats["pairs"] += sess.last_pairs
             stats["batches"] += -(-sess.last_pairs // sess.last_batch_size)
+        if profile:
+            e2.synchronize()
             rep = sess.last_replica
+            S = STAMPS
             for key, timer in rep.graph_events.items():
                 if timer is None:
                     continue
-                for b in range(timer.n // 4):
-                    for ph in range(3):
-                        stats["phase_ms"][ph].append(timer.elapsed(4 * b + ph, 4 * b + ph + 1))
+                for b in range(timer.n // S):
+                    o = S * b
+                    for name, (i0, i1) in PHASES.items():
+                        stats["phase_ms"].setdefault(name, []).append(timer.elapsed(o + i0, o + i1))
         return sess.last_pairs
 
     for i in range(args.warmup):
@@ -348,6 +355,14 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
     rows_updated = sess.rows_updated() - rows0
+    # kernel breakdown: one extra step after the timed region with device timestamps inside
+    # the CUDA graphs (kept out of the timed steps so they carry no event-record nodes)
+    rows_p0 = sess.rows_updated()
+    prof_t0 = time.perf_counter()
+    one_step(args.warmup + args.steps, False, profile=True)
+    prof_batches = -(-sess.last_pairs // sess.last_batch_size)
+    rows_per_batch_prof = (sess.rows_updated() - rows_p0) / max(prof_batches, 1)
+    prof_wall = time.perf_counter() - prof_t0
     ms = t_start.elapsed_time(t_end)
     ms_max = max_over_ranks(ms, world, dev)
     total_pairs = sum_over_ranks(float(pairs), world, dev)
@@ -389,17 +404,20 @@ def run_ours(args, rank, world, local):
     es = 4
     B = sess.last_batch_size
     n_batches = max(stats["batches"], 1)
-    U = rows_updated / n_batches  # unique (row, matrix) updates per batch
+    U = rows_per_batch_prof  # unique (row, matrix) updates per batch (profiled step)
     walk_ms = float(np.mean(stats["walk_ms"]))
     walk_bytes = 24 * stats["hops"] / args.steps + 8 * stats["walks"] / args.steps
-    ph = [float(np.mean(x)) if x else float("nan") for x in stats["phase_ms"]]
+    ph = {k_: float(np.mean(v_)) for k_, v_ in stats["phase_ms"].items()}
     pair_bytes = (2 + NEG) * DIM * es * B  # gathers of the 2+k rows (SURVEY §8d pair phase, first half)
     owner_bytes = (2 + NEG) * DIM * es * B + 8 * DIM * es * U  # scatter half + RowAdam rows
+    per = n_batches / args.steps
     kern = {
         "walk": {"ms": walk_ms, "bytes": walk_bytes, "per_step": 1},
-        "sgns_pair": {"ms": ph[0], "bytes": pair_bytes, "per_step": n_batches / args.steps},
-        "sgns_group_sort": {"ms": ph[1], "bytes": None, "per_step": n_batches / args.steps},
-        "sgns_owner_adam": {"ms": ph[2], "bytes": owner_bytes, "per_step": n_batches / args.steps},
+        "sgns_decode": {"ms": ph.get("decode", float("nan")), "bytes": None, "per_step": per},
+        "sgns_gather": {"ms": ph.get("gather", float("nan")), "bytes": pair_bytes, "per_step": per},
+        "sgns_group_sort(side stream, overlaps gather)": {"ms": ph.get("sort", float("nan")), "bytes": None,
+                                                           "per_step": per},
+        "sgns_owner_adam": {"ms": ph.get("owner", float("nan")), "bytes": owner_bytes, "per_step": per},
     }
     for k_, v_ in kern.items():
         v_["share_of_step"] = v_["ms"] * v_["per_step"] / (ms / args.steps)
@@ -407,7 +425,7 @@ def run_ours(args, rank, world, local):
         v_["frac"] = v_["gbs"] / peak if v_["gbs"] else None
     dom = max((k_ for k_ in kern if kern[k_]["bytes"]), key=lambda k_: kern[k_]["share_of_step"])
     batch_bytes = pair_bytes + owner_bytes
-    batch_ms = sum(x for x in ph if x == x)
+    batch_ms = ph.get("batch", float("nan"))
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
         "frac": kern[dom]["frac"], "traffic": None, "peak_source": peak_src,
@@ -416,8 +434,11 @@ def run_ours(args, rank, world, local):
         "sgns_batch": {"bytes": batch_bytes, "ms": batch_ms, "gbs": batch_bytes / (batch_ms * 1e-3) / 1e9,
                        "frac": batch_bytes / (batch_ms * 1e-3) / 1e9 / peak, "batch_pairs": B,
                        "unique_rows_per_batch": U},
-        "note": "achieved = SURVEY §8d algorithmic bytes per launch / mean CUDA-event launch time in the timed steps "
-                "(SGNS phases: events inside the CUDA graphs, last replay of each step). traffic: see profiles/",
+        "note": "achieved = SURVEY §8d algorithmic bytes per launch / mean CUDA-event launch time. walk: events "
+                "around the walk kernel in the timed steps; SGNS phases: device timestamps (external event records) "
+                "inside the CUDA graphs of one extra profiled step right after the timed region (last replay of each "
+                "graph). traffic: see profiles/",
+        "timed_unique_rows_per_batch": rows_updated / n_batches, "profiled_step_wall_s": prof_wall,
     }
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

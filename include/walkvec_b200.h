@@ -191,6 +191,10 @@ typedef struct WvSgnsBatch {
   const int32_t* pairs;
   const int64_t* perm;
   const int32_t* negative_table;
+  /* optional wv_timer_create handle: 7 stamps per batch from slot timer_base
+   * (start, decode end, gather end, join, owner end, sort start, sort end) */
+  void* timer;
+  int64_t timer_base;
 } WvSgnsBatch;
 
 int wv_sgns_init(int64_t vocab_size, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
@@ -211,10 +215,13 @@ int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, ui
 int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, void* stream);
 int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
                                       int precision);
+/* zero the workspace's persistent per-row counters: once after allocating it */
+int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size, int negatives,
+                           int64_t batch, int precision, void* stream);
 int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream);
-#define WV_PHASE_PAIRS 1  /* gather rows, dots, coefficients, grouping keys, batch loss */
-#define WV_PHASE_GROUP 2  /* stable radix sort of contributions by row + segment heads */
-#define WV_PHASE_UPDATE 4 /* one warp per unique row: slot-ordered sum + Adam */
+#define WV_PHASE_PAIRS 1  /* decode pair/negative rows; gather rows, dots, coefficients, batch loss */
+#define WV_PHASE_GROUP 2  /* group contribution slots by destination row (no sort) */
+#define WV_PHASE_UPDATE 4 /* per unique row: slot-ordered sum + RowAdam */
 #define WV_PHASE_ALL 7
 int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int phases,
                          void* stream);

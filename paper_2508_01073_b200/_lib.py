@@ -99,6 +99,8 @@ class WvSgnsBatch(C.Structure):
         ("pairs", C.c_void_p),
         ("perm", C.c_void_p),
         ("negative_table", C.c_void_p),
+        ("timer", C.c_void_p),
+        ("timer_base", C.c_int64),
     ]
 
 
@@ -145,6 +147,7 @@ SIGNATURES = {
     "wv_candidates": (I32, [P, I64, I64, P, P, P, P, I64, P]),
     "wv_sgns_epoch_begin": (I32, [P, I64, I64, P]),
     "wv_sgns_batch_workspace_bytes": (I64, [I64, I32, I32, I64, I32]),
+    "wv_sgns_workspace_init": (I32, [P, I64, I64, I32, I32, I64, I32, P]),
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
     "wv_replica_delta": (I32, [P, P, I64, I32, P, P]),

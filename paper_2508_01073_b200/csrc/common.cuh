@@ -250,6 +250,12 @@ void note_launches(int n);
     }                                                                           \
   } while (0)
 
+#define WV_CUDA_RC(expr)    \
+  do {                      \
+    int _rc = (expr);       \
+    if (_rc) return _rc;    \
+  } while (0)
+
 #define WV_LAUNCH_CHECK()                                                          \
   do {                                                                             \
     ::wv::note_launches(1);                                                        \

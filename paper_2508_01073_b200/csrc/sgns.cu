@@ -18,6 +18,7 @@
 // order; one warp per unique row then sums its contributions and applies
 // Adam in place.  No float atomics: results are deterministic run to run.
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "common.cuh"
@@ -209,33 +210,47 @@ struct PairArgs {
   void* U;
   void* G;
   void* coef;
-  uint32_t* keys;
-  uint32_t* vals;
+  uint32_t* cnt;   // [2V] per-row item count / list cursor; all zero between batches
+  uint32_t* uniq;  // [items] unique row keys of the batch
+  uint32_t* gctr;  // grouping counters (GC_*)
+  int32_t* idx;    // [B, 2+k] centre, context, negatives
   double* partials;
   WvSgnsDevState* state;
-  uint32_t* seg_count;
 };
 
-template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(kPairThreads) sgns_pair_kernel(PairArgs A, const T* __restrict__ in,
-                                                                   const T* __restrict__ out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int d = A.d, k = A.k;
-  const int C = d / EPC;
+// ------------------------------------------------------------ grouping ---
+// Contributions are grouped by destination row without a sort.  A row key is
+// the input-matrix row r (key r) or the output-matrix row r (key V + r); an
+// item's slot is its position in the reference's gradient stacking order:
+// centre b -> b, context b -> B + b, negative j of pair b -> 2B + bk + j
+// (the order np.add.at applies them, w2v.py:287-295, 407-416).
+//   decode : cnt[key] += 1 per item; the first item of a key claims a unique id
+//   group_segments : per unique key, reserve cnt[key] list slots (cnt[key]
+//            becomes the list cursor), advance the row's RowAdam step, split
+//            light / heavy rows
+//   group_place : each item appends its slot to its row's list
+// The list order inside a row is arbitrary; the owner kernels restore slot
+// order (warp ranking / CTA radix sort) before summing, so results are
+// deterministic, and reset cnt[key] to 0 for the next batch.
+enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3 };
+
+__device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
+  if (atomicAdd(A.cnt + key, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = key;
+}
+
+// Phase 1a, thread per pair: the batch's row indices (centre, context, k
+// negatives) and the grouping-sort input.  Pair decode (Feistel position ->
+// length class -> walk -> window slot) is a chain of dependent L2 reads, so
+// it runs here with one thread per pair (latency hidden by parallelism)
+// instead of serialising inside the gather warps.
+__global__ void __launch_bounds__(256) sgns_decode_kernel(PairArgs A) {
+  const int k = A.k;
   const int64_t B = A.B;
   const int64_t lo = A.state->lo;
   const uint64_t epoch = (uint64_t)A.state->epoch;
-  T* U = (T*)A.U;
-  T* G = (T*)A.G;
-  T* coef = (T*)A.coef;
-  const T invB = (T)1 / (T)B;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *A.seg_count = 0;
-
   Feistel fs;
   if (A.mode == WV_PAIRS_NATIVE) fs = make_feistel(A.seed, epoch, A.N);
-
-  double loss_acc = 0.0;
-  for (int64_t b = blockIdx.x * (int64_t)kPairWarps + warp; b < B; b += (int64_t)gridDim.x * kPairWarps) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pos = lo + b;
     int32_t center, context;
     if (A.mode == WV_PAIRS_NATIVE) {
@@ -261,39 +276,284 @@ __global__ void __launch_bounds__(kPairThreads) sgns_pair_kernel(PairArgs A, con
       center = A.pairs[2 * pi];
       context = A.pairs[2 * pi + 1];
     }
-    // native negatives: Philox4x32 counter (epoch, position, call)
+    int32_t* row = A.idx + b * (2 + k);
+    row[0] = center;
+    row[1] = context;
+    group_claim(A, (uint32_t)center);
+    group_claim(A, (uint32_t)(context + A.V));
+    // native negatives: Philox4x32 counter (position, epoch, call), two draws per call
     uint32_t rnd[4];
-    int rnd_left = 0;
-    int call = 0;
+    for (int j = 0; j < k; ++j) {
+      int32_t neg;
+      if (A.mode == WV_PAIRS_NATIVE) {
+        if ((j & 1) == 0) {
+          rnd[0] = (uint32_t)pos;
+          rnd[1] = (uint32_t)((uint64_t)pos >> 32);
+          rnd[2] = (uint32_t)epoch;
+          rnd[3] = (uint32_t)(j >> 1);
+          philox4x32_10(rnd, (uint32_t)A.seed ^ 0xA5A5F00Du, (uint32_t)(A.seed >> 32) ^ 0x3C6EF372u);
+        }
+        const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
+        const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)A.n_candidates);
+        neg = A.candidates ? A.candidates[ci] : (int32_t)ci;
+      } else {
+        neg = A.negatives[pos * k + j];
+      }
+      row[2 + j] = neg;
+      group_claim(A, (uint32_t)(neg + A.V));
+    }
+  }
+}
 
+// ------------------------------------------------ bulk-copy (TMA) gather --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// one row, global -> shared, completion counted on `bar` (cp.async.bulk -> UBLKCP)
+__device__ __forceinline__ void bulk_row_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T log1pexp_t(T x);
+template <>
+__device__ __forceinline__ double log1pexp_t<double>(double x) { return log1pexp(x); }
+template <>
+__device__ __forceinline__ float log1pexp_t<float>(float x) { return x > 0.f ? x + log1pf(__expf(-x)) : log1pf(__expf(x)); }
+
+// Batch loss of one block -> partials; the last block to finish folds the
+// partials in block order (deterministic) into the device state.
+__device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double block_sum) {
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    A.partials[blockIdx.x] = block_sum;
+    __threadfence();
+    const unsigned done = atomicAdd(&A.state->block_counter, 1u);
+    is_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0;
+    for (unsigned i = 0; i < gridDim.x; ++i) s += ((volatile double*)A.partials)[i];
+    WvSgnsDevState* st = A.state;
+    st->block_counter = 0;
+    const double batch_loss = s / (double)A.B;
+    if (!isfinite(batch_loss) && st->diverged_batch < 0) {
+      st->diverged_batch = st->batch;
+      st->diverged_epoch = st->epoch;
+    }
+    st->epoch_loss_sum += batch_loss * (double)A.B;
+    st->epoch_count += A.B;
+    st->last_batch_loss = batch_loss;
+  }
+}
+
+constexpr int kBulkWarps = 4;
+constexpr int kBulkThreads = kBulkWarps * 32;
+
+// Phase 1b (default path): warp per pair with the 2+k rows fetched by
+// cp.async.bulk into a per-warp two-stage shared-memory ring.  Lane j issues
+// row j's copy, so the whole pair (7 x 800 B at d=200) is in flight at once
+// and the next pair's rows land while this pair computes; no row data is held
+// in registers across the wait, which keeps occupancy up.  Lanes 0..k each
+// evaluate one loss term (the reference's float64 logaddexp, w2v.py:262-273).
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs A, const T* __restrict__ in,
+                                                                         const T* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = A.d, k = A.k;
+  const int R = 2 + k;
+  const int C = d / EPC;
+  const int64_t B = A.B;
+  const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [warps][2]
+  T* ring = reinterpret_cast<T*>(smem_raw + 128) + (size_t)warp * 2 * R * d;
+  uint64_t* mybar = bars + 2 * warp;
+  if (lane == 0) {
+    mbar_init(mybar, 1);
+    mbar_init(mybar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  T* U = (T*)A.U;
+  T* G = (T*)A.G;
+  T* coef = (T*)A.coef;
+  const T invB = (T)1 / (T)B;
+  const int64_t stride = (int64_t)gridDim.x * kBulkWarps;
+  int64_t b = blockIdx.x * (int64_t)kBulkWarps + warp;
+  // prologue: stage 0 <- first pair
+  auto issue = [&](int64_t pb, int stage) {
+    T* dst = ring + (size_t)stage * R * d;
+    int32_t r = 0;
+    if (lane < R) r = __ldg(A.idx + pb * R + lane);
+    if (lane == 0) mbar_arrive_expect_tx(mybar + stage, row_bytes * (uint32_t)R);
+    __syncwarp();
+    if (lane < R) {
+      const T* src = (lane == 0 ? in : out) + (int64_t)r * d;
+      bulk_row_g2s(dst + (size_t)lane * d, src, row_bytes, mybar + stage);
+    }
+  };
+  if (b < B) issue(b, 0);
+  double loss_acc = 0.0;
+  uint32_t phase[2] = {0u, 0u};
+  for (int it = 0; b < B; ++it, b += stride) {
+    const int stage = it & 1;
+    const int64_t nb = b + stride;
+    if (nb < B) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nb, stage ^ 1);
+    }
+    while (!mbar_try_wait(mybar + stage, phase[stage])) {
+    }
+    phase[stage] ^= 1u;
+    const T* rows = ring + (size_t)stage * R * d;
+    Chunk<T, EPC> u[MAXC];
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int c = lane + 32 * q;
+      if (c < C) u[q] = *reinterpret_cast<const Chunk<T, EPC>*>(rows + c * EPC);
+    }
+    // dot j = <u, row 1+j> (j = 0: context, j >= 1: negative j-1); lane j keeps dot j
+    T mydot = 0;
+    for (int j = 0; j <= k; ++j) {
+      const T* rj = rows + (size_t)(1 + j) * d;
+      T dot = 0;
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int c = lane + 32 * q;
+        if (c < C) {
+          const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rj + c * EPC);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) dot += u[q].v[e] * x.v[e];
+        }
+      }
+      dot = warp_sum(dot);
+      if (lane == j) mydot = dot;
+    }
+    // lane j: loss term and coefficient of dot j
+    T mycoef = 0;
+    if (lane <= k) {
+      loss_acc += (double)log1pexp_t<T>(lane == 0 ? -mydot : mydot);
+      const T sg = T(1) / (T(1) + exp_t(-mydot));
+      mycoef = (lane == 0 ? sg - T(1) : sg) * invB;
+      coef[b * (k + 1) + lane] = mycoef;
+    }
+    const T gpos = __shfl_sync(0xffffffffu, mycoef, 0);
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int c = lane + 32 * q;
+      Chunk<T, EPC> acc;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) acc.v[e] = 0;
+      for (int j = 1; j <= k; ++j) {
+        const T gneg = __shfl_sync(0xffffffffu, mycoef, j);
+        if (c < C) {
+          const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)(1 + j) * d + c * EPC);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) acc.v[e] = add_rn(acc.v[e], mul_rn(gneg, x.v[e]));
+        }
+      }
+      if (c < C) {
+        const Chunk<T, EPC> v = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)d + c * EPC);
+        Chunk<T, EPC> gg;
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) gg.v[e] = add_rn(mul_rn(gpos, v.v[e]), acc.v[e]);
+        st_chunk<T, EPC>(G + b * d + c * EPC, gg);
+        st_chunk<T, EPC>(U + b * d + c * EPC, u[q]);
+      }
+    }
+    __syncwarp();
+  }
+  // block loss: lanes -> warp -> block (fixed order)
+  loss_acc = warp_sum(loss_acc);
+  __shared__ double wl[kBulkWarps];
+  if (lane == 0) wl[warp] = loss_acc;
+  __syncthreads();
+  double blk = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kBulkWarps; ++w) blk += wl[w];
+  finish_batch_loss(A, blk);
+}
+
+// Phase 1b, warp per pair: gather the 2+k rows with 16-byte loads -- every
+// load of a negative group is issued before the first dot product so each
+// lane keeps several independent row chunks in flight -- then the (1+k) dots
+// (warp shuffles), the loss, the per-pair coefficients and two [B,d] rows:
+// the centre row u and its gradient g_u = gpos v + sum_j gneg_j n_j.
+template <typename T, int EPC, int MAXC, int NG>
+__global__ void __launch_bounds__(kPairThreads) sgns_gather_kernel(PairArgs A, const T* __restrict__ in,
+                                                                     const T* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = A.d, k = A.k;
+  const int C = d / EPC;
+  const int64_t B = A.B;
+  T* U = (T*)A.U;
+  T* G = (T*)A.G;
+  T* coef = (T*)A.coef;
+  const T invB = (T)1 / (T)B;
+  double loss_acc = 0.0;
+  for (int64_t b = blockIdx.x * (int64_t)kPairWarps + warp; b < B; b += (int64_t)gridDim.x * kPairWarps) {
+    const int32_t my = lane < 2 + k ? __ldg(A.idx + b * (2 + k) + lane) : 0;
+    const int32_t center = __shfl_sync(0xffffffffu, my, 0);
+    const int32_t context = __shfl_sync(0xffffffffu, my, 1);
     const T* urow = in + (int64_t)center * d;
     const T* vrow = out + (int64_t)context * d;
-    Chunk<T, EPC> u[MAXC], g[MAXC], acc[MAXC];
-    T dot = 0;
+    Chunk<T, EPC> u[MAXC], g[MAXC], nv[NG][MAXC];
+    const int g0 = k < NG ? k : NG;
 #pragma unroll
     for (int q = 0; q < MAXC; ++q) {
       const int c = lane + 32 * q;
       if (c < C) {
         u[q] = ld_chunk<T, EPC>(urow + c * EPC);
-        Chunk<T, EPC> v = ld_chunk<T, EPC>(vrow + c * EPC);
-        g[q] = v;  // keep v until gpos is known
+        g[q] = ld_chunk<T, EPC>(vrow + c * EPC);
+      }
+    }
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) {
-          dot += u[q].v[e] * v.v[e];
-          acc[q].v[e] = 0;
+    for (int j = 0; j < NG; ++j) {
+      const int32_t nj = __shfl_sync(0xffffffffu, my, 2 + j);
+      if (j < g0) {
+        const T* nrow = out + (int64_t)nj * d;
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q) {
+          const int c = lane + 32 * q;
+          if (c < C) nv[j][q] = ld_chunk<T, EPC>(nrow + c * EPC);
         }
+      }
+    }
+    T dot = 0;
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int c = lane + 32 * q;
+      if (c < C) {
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) dot += u[q].v[e] * g[q].v[e];
       }
     }
     const T pos_logit = warp_sum(dot);
     double l = log1pexp(-(double)pos_logit);
     const T gpos = (T(1) / (T(1) + exp_t(-pos_logit)) - T(1)) * invB;
-    if (lane == 0) {
-      coef[b * (k + 1)] = gpos;
-      A.keys[b] = (uint32_t)center;
-      A.vals[b] = (uint32_t)b;
-      A.keys[B + b] = (uint32_t)(context + A.V);
-      A.vals[B + b] = (uint32_t)(B + b);
-    }
+    if (lane == 0) coef[b * (k + 1)] = gpos;
 #pragma unroll
     for (int q = 0; q < MAXC; ++q) {
       const int c = lane + 32 * q;
@@ -302,52 +562,52 @@ __global__ void __launch_bounds__(kPairThreads) sgns_pair_kernel(PairArgs A, con
         for (int e = 0; e < EPC; ++e) g[q].v[e] = mul_rn(gpos, g[q].v[e]);
       }
     }
-    for (int j = 0; j < k; ++j) {
-      int32_t neg;
-      if (A.mode == WV_PAIRS_NATIVE) {
-        if (rnd_left == 0) {
-          rnd[0] = (uint32_t)pos;
-          rnd[1] = (uint32_t)((uint64_t)pos >> 32);
-          rnd[2] = (uint32_t)epoch;
-          rnd[3] = (uint32_t)call++;
-          philox4x32_10(rnd, (uint32_t)A.seed ^ 0xA5A5F00Du, (uint32_t)(A.seed >> 32) ^ 0x3C6EF372u);
-          rnd_left = 2;
-        }
-        const uint64_t r64 = ((uint64_t)rnd[2 * (2 - rnd_left) + 1] << 32) | rnd[2 * (2 - rnd_left)];
-        --rnd_left;
-        const int64_t idx = (int64_t)mulhi64(r64, (uint64_t)A.n_candidates);
-        neg = A.candidates ? A.candidates[idx] : (int32_t)idx;
-      } else {
-        neg = A.negatives[pos * k + j];
-      }
-      const T* nrow = out + (int64_t)neg * d;
-      Chunk<T, EPC> nv[MAXC];
-      T nd = 0;
+    Chunk<T, EPC> acc[MAXC];
 #pragma unroll
-      for (int q = 0; q < MAXC; ++q) {
-        const int c = lane + 32 * q;
-        if (c < C) {
-          nv[q] = ld_chunk<T, EPC>(nrow + c * EPC);
+    for (int q = 0; q < MAXC; ++q)
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) nd += u[q].v[e] * nv[q].v[e];
+      for (int e = 0; e < EPC; ++e) acc[q].v[e] = 0;
+    for (int j0 = 0; j0 < k; j0 += NG) {
+      const int gn = k - j0 < NG ? k - j0 : NG;
+      if (j0 > 0) {  // later negative groups (k > NG): issue the whole group, then reduce
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+          const int32_t nj = __shfl_sync(0xffffffffu, my, 2 + ((j0 + j) < k ? j0 + j : 0));
+          if (j < gn) {
+            const T* nrow = out + (int64_t)nj * d;
+#pragma unroll
+            for (int q = 0; q < MAXC; ++q) {
+              const int c = lane + 32 * q;
+              if (c < C) nv[j][q] = ld_chunk<T, EPC>(nrow + c * EPC);
+            }
+          }
         }
       }
-      const T neg_logit = warp_sum(nd);
-      l += log1pexp((double)neg_logit);
-      const T gneg = (T(1) / (T(1) + exp_t(-neg_logit))) * invB;
 #pragma unroll
-      for (int q = 0; q < MAXC; ++q) {
-        const int c = lane + 32 * q;
-        if (c < C) {
+      for (int j = 0; j < NG; ++j) {
+        if (j < gn) {
+          T nd = 0;
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) acc[q].v[e] = add_rn(acc[q].v[e], mul_rn(gneg, nv[q].v[e]));
+          for (int q = 0; q < MAXC; ++q) {
+            const int c = lane + 32 * q;
+            if (c < C) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) nd += u[q].v[e] * nv[j][q].v[e];
+            }
+          }
+          const T neg_logit = warp_sum(nd);
+          l += log1pexp((double)neg_logit);
+          const T gneg = (T(1) / (T(1) + exp_t(-neg_logit))) * invB;
+#pragma unroll
+          for (int q = 0; q < MAXC; ++q) {
+            const int c = lane + 32 * q;
+            if (c < C) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) acc[q].v[e] = add_rn(acc[q].v[e], mul_rn(gneg, nv[j][q].v[e]));
+            }
+          }
+          if (lane == 0) coef[b * (k + 1) + 1 + j0 + j] = gneg;
         }
-      }
-      if (lane == 0) {
-        coef[b * (k + 1) + 1 + j] = gneg;
-        const int64_t slot = B + b * k + j;
-        A.keys[B + slot] = (uint32_t)(neg + A.V);
-        A.vals[B + slot] = (uint32_t)(B + slot);
       }
     }
 #pragma unroll
@@ -395,24 +655,87 @@ __global__ void __launch_bounds__(kPairThreads) sgns_pair_kernel(PairArgs A, con
   }
 }
 
-// Segment heads of the sorted contribution keys; also advances the batch cursor.
-__global__ void seg_heads(const uint32_t* __restrict__ keys, int64_t n, int64_t* __restrict__ seg_start,
-                          uint32_t* __restrict__ seg_count, WvSgnsDevState* state, int64_t B) {
+// Rows with more than kLightMax contributions in a batch (predicates, hub
+// entities) go to the CTA-per-row kernel; the rest to the warp-per-row one.
+constexpr int kLightMax = 16;
+constexpr int kHeavyThreads = 256;
+
+// One record per unique (matrix, row) of the batch, built by group_segments.
+struct Segment {
+  uint32_t start;  // first entry of the row's slot list
+  uint32_t len;    // contributions
+  uint32_t key;    // row key (input row r, or V + output row r)
+  uint32_t pad;
+  double bc1;      // Adam bias corrections 1 - b1^t, 1 - b2^t with the row's new step t
+  double bc2;
+};
+
+__global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __restrict__ cnt, uint32_t* gctr,
+                               int64_t V, int sparse, int32_t* __restrict__ steps_in, int32_t* __restrict__ steps_out,
+                               Segment* __restrict__ segs, Segment* __restrict__ heavy, int64_t max_unique) {
   const int lane = threadIdx.x & 31;
+  const uint32_t nu = *(volatile uint32_t*)(gctr + GC_UNIQUE);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool head = i < n && (i == 0 || keys[i] != keys[i - 1]);
-    uint32_t m = __ballot_sync(0xffffffffu, head);
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nu && base < max_unique; base += stride) {
+    const int64_t u = base + threadIdx.x;
+    const bool ok = u < nu;
+    const uint32_t key = ok ? uniq[u] : 0u;
+    const uint32_t len = ok ? cnt[key] : 0u;
+    // warp-aggregated list reservation
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
     uint32_t wbase = 0;
-    if (lane == 0 && m) wbase = atomicAdd(seg_count, (uint32_t)__popc(m));
-    wbase = __shfl_sync(0xffffffffu, wbase, 0);
-    if (head) seg_start[wbase + __popc(m & ((1u << lane) - 1u))] = i;
+    if (lane == 31) wbase = atomicAdd(gctr + GC_TOTAL, incl);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    const uint32_t start = wbase + incl - len;
+    const bool is_heavy = ok && len > (uint32_t)kLightMax;
+    const uint32_t ml = __ballot_sync(0xffffffffu, ok && !is_heavy);
+    const uint32_t mh = __ballot_sync(0xffffffffu, is_heavy);
+    uint32_t lb = 0, hb = 0;
+    if (lane == 0 && ml) lb = atomicAdd(gctr + GC_LIGHT, (uint32_t)__popc(ml));
+    if (lane == 0 && mh) hb = atomicAdd(gctr + GC_HEAVY, (uint32_t)__popc(mh));
+    lb = __shfl_sync(0xffffffffu, lb, 0);
+    hb = __shfl_sync(0xffffffffu, hb, 0);
+    if (ok) {
+      cnt[key] = start;  // becomes the placement cursor
+      Segment sg;
+      sg.start = start;
+      sg.len = len;
+      sg.key = key;
+      sg.pad = 0;
+      sg.bc1 = sg.bc2 = 1.0;
+      if (sparse) {
+        const bool side_out = key >= (uint32_t)V;
+        int32_t* steps = side_out ? steps_out : steps_in;
+        const int64_t row = side_out ? (int64_t)key - V : (int64_t)key;
+        const int t = steps[row] + 1;
+        steps[row] = t;
+        sg.bc1 = 1.0 - pow(0.9, (double)t);
+        sg.bc2 = 1.0 - pow(0.999, (double)t);
+      }
+      const uint32_t below = (1u << lane) - 1u;
+      if (is_heavy)
+        heavy[hb + __popc(mh & below)] = sg;
+      else
+        segs[lb + __popc(ml & below)] = sg;
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    state->lo += B;
-    state->batch += 1;
-    state->step += 1;
+}
+
+// every item appends its slot to its row's list
+__global__ void group_place(const int32_t* __restrict__ idx, int64_t B, int k, int64_t V, uint32_t* __restrict__ cnt,
+                            uint32_t* __restrict__ list) {
+  const int64_t items = B * (2 + k);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < items; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / (2 + k);
+    const int j = (int)(i - b * (2 + k));
+    const uint32_t key = (uint32_t)idx[i] + (j == 0 ? 0u : (uint32_t)V);
+    const uint32_t slot = (uint32_t)(j == 0 ? b : (j == 1 ? B + b : 2 * B + b * k + (j - 2)));
+    list[atomicAdd(cnt + key, 1u)] = slot;
   }
 }
 
@@ -422,10 +745,13 @@ struct OwnerArgs {
   int k;
   int64_t B;
   int64_t n_items;
-  const uint32_t* keys;
-  const uint32_t* vals;
-  const int64_t* seg_start;
-  const uint32_t* seg_count;
+  const uint32_t* list;  // per-row slot lists (arbitrary order inside a row)
+  uint32_t* list_tmp;    // scratch for the heavy rows' slot sort
+  uint32_t* cnt;         // reset to 0 per row once consumed
+  int slot_bits;         // bits of the largest slot (2B + Bk - 1)
+  const Segment* segs;
+  const Segment* heavy;
+  const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
   const void* U;
   const void* G;
   const void* coef;
@@ -435,8 +761,6 @@ struct OwnerArgs {
   void* v_in;
   void* m_out;
   void* v_out;
-  int32_t* steps_in;
-  int32_t* steps_out;
   uint8_t* touched_in;
   uint8_t* touched_out;
   uint8_t* modified_in;
@@ -448,113 +772,314 @@ struct OwnerArgs {
   WvSgnsDevState* state;
 };
 
+// Sorted contribution value v -> (source row, coefficient): input-matrix rows
+// take the pair's centre gradient row G[b] (coefficient 1); output-matrix rows
+// take coef * U[b] (the context's gpos or negative j's gneg).
+template <typename T>
+__device__ __forceinline__ void contribution(uint32_t v, bool side_out, int64_t B, int k, int d, const T* U,
+                                             const T* G, const T* coef, const T*& src, T& c) {
+  if (!side_out) {
+    src = G + (int64_t)v * d;
+    c = 1;
+    return;
+  }
+  const int64_t s = (int64_t)v - B;
+  int64_t pp, j;
+  if (s < B) {
+    pp = s;
+    j = 0;
+  } else {
+    pp = (s - B) / k;
+    j = 1 + (s - B) - pp * k;
+  }
+  src = U + pp * d;
+  c = __ldg(coef + pp * (k + 1) + j);
+}
+
+// Phase 3: one warp per (unique row, 32-chunk slice of the row): sum the row's
+// contributions in slot order (the order np.add.at applies them, w2v.py:415)
+// and apply RowAdam in place.  One 16-byte chunk per lane keeps registers low
+// so many warps are resident; the optimizer-state loads are issued before the
+// contribution walk so their DRAM latency overlaps it.
 template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(kOwnerThreads) sgns_owner_kernel(OwnerArgs A) {
+__global__ void __launch_bounds__(kOwnerThreads, 4) sgns_owner_kernel(OwnerArgs A) {
   const int lane = threadIdx.x & 31;
-  const int warps_total = gridDim.x * (kOwnerThreads / 32);
-  const int gw = blockIdx.x * (kOwnerThreads / 32) + (threadIdx.x >> 5);
+  const int64_t warps_total = (int64_t)gridDim.x * (kOwnerThreads / 32);
+  const int64_t gw = blockIdx.x * (int64_t)(kOwnerThreads / 32) + (threadIdx.x >> 5);
   const int d = A.d, k = A.k;
   const int C = d / EPC;
   const int64_t B = A.B;
   const uint32_t nseg = *A.seg_count;
-  if (blockIdx.x == 0 && threadIdx.x == 0) A.state->rows_updated += nseg;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the batch is consumed: advance the cursor (read by the next batch's decode)
+    WvSgnsDevState* st = A.state;
+    st->rows_updated += nseg;
+    st->lo += B;
+    st->batch += 1;
+    st->step += 1;
+  }
   const T* U = (const T*)A.U;
   const T* G = (const T*)A.G;
   const T* coef = (const T*)A.coef;
   const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
   const T lr = (T)A.lr;
-  for (uint32_t sg = gw; sg < nseg; sg += warps_total) {
-    const int64_t start = A.seg_start[sg];
-    const uint32_t key = A.keys[start];
+  const int64_t slots = (int64_t)nseg * MAXC;
+  for (int64_t slot = gw; slot < slots; slot += warps_total) {
+    const int64_t sgi = slot / MAXC;
+    const int cc = (int)(slot - sgi * MAXC) * 32 + lane;
+    const Segment sg = A.segs[sgi];
+    const uint32_t key = sg.key;
     const bool side_out = key >= (uint32_t)A.V;
     const int64_t row = side_out ? (int64_t)key - A.V : (int64_t)key;
+    const bool active = cc < C;
+    // the row's (<= kLightMax) slots, ranked so they are summed in slot order
+    const uint32_t myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
+    int myrank = 0;
+    for (int j = 0; j < (int)sg.len; ++j) myrank += __shfl_sync(0xffffffffu, myslot, j) < myslot;
+    T* P = (T*)(side_out ? A.out : A.in);
+    T* M = (T*)(side_out ? A.m_out : A.m_in);
+    T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    const int64_t o = row * d + (int64_t)cc * EPC;
+    Chunk<T, EPC> p, m, vv, g;
+    if (A.sparse && active) {
+      p = ld_chunk_rw<T, EPC>(P + o);
+      m = ld_chunk_rw<T, EPC>(M + o);
+      vv = ld_chunk_rw<T, EPC>(Vv + o);
+    }
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) g.v[e] = 0;
+    // contributions in groups of 4: all loads of a group are issued before the
+    // (slot-ordered) adds, so a row's walk costs len/4 dependent round trips
+    for (uint32_t i0 = 0; i0 < sg.len; i0 += 4) {
+      const int nq = (int)min(4u, sg.len - i0);
+      const T* src[4];
+      T c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t owner = __ballot_sync(0xffffffffu, myrank == (int)i0 + q && lane < (int)sg.len);
+        const uint32_t v = __shfl_sync(0xffffffffu, myslot, owner ? __ffs(owner) - 1 : 0);
+        src[q] = nullptr;
+        c[q] = 0;
+        if (q < nq) contribution<T>(v, side_out, B, k, d, U, G, coef, src[q], c[q]);
+      }
+      Chunk<T, EPC> x[4];
+      if (active) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < nq) x[q] = ld_chunk<T, EPC>(src[q] + cc * EPC);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < nq) {
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) g.v[e] = add_rn(g.v[e], side_out ? mul_rn(c[q], x[q].v[e]) : x[q].v[e]);
+          }
+      }
+    }
+    if (!A.sparse) {
+      T* D = (T*)(side_out ? A.dense_g_out : A.dense_g_in);
+      if (active) st_chunk<T, EPC>(D + o, g);
+      if (lane == 0 && cc == 0) {
+        (side_out ? A.touched_out : A.touched_in)[row] = 1;
+        A.cnt[key] = 0;
+      }
+      continue;
+    }
+    const T bc1 = (T)sg.bc1, bc2 = (T)sg.bc2;
+    bool changed = false;
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+        const T gr = g.v[e];
+        m.v[e] = add_rn(mul_rn(b1, m.v[e]), mul_rn(omb1, gr));
+        vv.v[e] = add_rn(mul_rn(b2, vv.v[e]), mul_rn(mul_rn(omb2, gr), gr));
+        const T mh = div_rn(m.v[e], bc1);
+        const T vh = div_rn(vv.v[e], bc2);
+        const T upd = div_rn(mul_rn(lr, mh), add_rn(sqrt_rn(vh), eps));
+        const T np_ = sub_rn(p.v[e], upd);
+        changed |= (np_ != p.v[e]) || (np_ != np_);
+        p.v[e] = np_;
+      }
+      st_chunk<T, EPC>(P + o, p);
+      st_chunk<T, EPC>(M + o, m);
+      st_chunk<T, EPC>(Vv + o, vv);
+    }
+    changed = __any_sync(0xffffffffu, changed);
+    if (lane == 0) {
+      if (cc == 0) {
+        (side_out ? A.touched_out : A.touched_in)[row] = 1;
+        A.cnt[key] = 0;
+      }
+      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+    }
+  }
+}
+
+// Stable LSD radix sort (8-bit digits) of n slots by one CTA of kHeavyThreads
+// threads: a ping-pongs with tmp; returns the buffer holding the result.  Per
+// tile of kHeavyThreads items each warp ranks equal digits with match_any and
+// the per-(warp, digit) counts are prefixed in warp order, so ties keep input
+// order (slots are distinct anyway; stability keeps it a pure permutation).
+__device__ uint32_t* cta_sort_slots(uint32_t* a, uint32_t* tmp, uint32_t n, int bits,
+                                    uint32_t (*cnt)[256]) {
+  constexpr int NW = kHeavyThreads / 32;
+  __shared__ uint32_t base[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int shift = 0; shift < bits; shift += 8) {
+    // global digit histogram -> exclusive bases
+    for (int t = threadIdx.x; t < 256; t += kHeavyThreads) base[t] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += kHeavyThreads) atomicAdd(&base[(a[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t carry = 0;
+      for (int c0 = 0; c0 < 256; c0 += 32) {
+        const uint32_t v = base[c0 + lane];
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += x;
+        }
+        base[c0 + lane] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    __syncthreads();
+    for (uint32_t t0 = 0; t0 < n; t0 += kHeavyThreads) {
+      const uint32_t i = t0 + threadIdx.x;
+      const bool ok = i < n;
+      const uint32_t x = ok ? a[i] : 0u;
+      const uint32_t dg = ok ? (x >> shift) & 255u : 256u + lane;  // unique dummy digit
+      for (int t = threadIdx.x; t < NW * 256; t += kHeavyThreads) cnt[t / 256][t % 256] = 0;
+      __syncthreads();
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+      if (ok && rank == 0) cnt[warp][dg] = __popc(peers);
+      __syncthreads();
+      for (int t = threadIdx.x; t < 256; t += kHeavyThreads) {
+        uint32_t off = base[t];
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t c = cnt[w][t];
+          cnt[w][t] = off;
+          off += c;
+        }
+        base[t] = off;
+      }
+      __syncthreads();
+      if (ok) tmp[cnt[warp][dg] + rank] = x;
+      __syncthreads();
+    }
+    uint32_t* sw = a;
+    a = tmp;
+    tmp = sw;
+    __syncthreads();
+  }
+  return a;
+}
+
+// Phase 3b: one CTA per heavy row.  Warp w sums the w-th contiguous eighth of
+// the row's contributions (slot order inside each part), the parts are added
+// in part order through shared memory (a fixed two-level order, so the result
+// is deterministic), then the threads apply RowAdam element-parallel.
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) {
+  constexpr int W = kHeavyThreads / 32;
+  extern __shared__ unsigned char smem_raw[];
+  T* part = reinterpret_cast<T*>(smem_raw);  // [W][d]
+  __shared__ uint32_t sort_hist[kHeavyThreads / 32][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = A.d, k = A.k;
+  const int C = d / EPC;
+  const int64_t B = A.B;
+  const uint32_t nh = A.seg_count[1];
+  const T* U = (const T*)A.U;
+  const T* G = (const T*)A.G;
+  const T* coef = (const T*)A.coef;
+  const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
+  const T lr = (T)A.lr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) A.state->rows_updated += nh;
+  for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const Segment sg = A.heavy[h];
+    const uint32_t key = sg.key;
+    const bool side_out = key >= (uint32_t)A.V;
+    const int64_t row = side_out ? (int64_t)key - A.V : (int64_t)key;
+    // restore slot order of the row's list (stable LSD radix sort, ping-pong
+    // with the scratch list at the same offsets)
+    const uint32_t* sorted = cta_sort_slots(const_cast<uint32_t*>(A.list) + sg.start, A.list_tmp + sg.start, sg.len,
+                                            A.slot_bits, sort_hist);
+    const uint32_t per = (sg.len + W - 1) / W;
+    const uint32_t lo = min(sg.len, per * warp), hi = min(sg.len, per * (warp + 1));
     Chunk<T, EPC> g[MAXC];
 #pragma unroll
     for (int q = 0; q < MAXC; ++q)
 #pragma unroll
       for (int e = 0; e < EPC; ++e) g[q].v[e] = 0;
-    for (int64_t i = start; i < A.n_items && A.keys[i] == key; ++i) {
-      const uint32_t v = A.vals[i];
-      const T* src;
-      T c;
-      if (!side_out) {
-        src = G + (int64_t)v * d;
-        c = 1;
-      } else {
-        const int64_t s = (int64_t)v - B;
-        int64_t p, j;
-        if (s < B) {
-          p = s;
-          j = 0;
-        } else {
-          p = (s - B) / k;
-          j = 1 + (s - B) - p * k;
-        }
-        src = U + p * d;
-        c = coef[p * (k + 1) + j];
+    for (uint32_t i0 = lo; i0 < hi; i0 += 4) {
+      const int nq = (int)min(4u, hi - i0);
+      const T* src[4];
+      T c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        src[q] = nullptr;
+        c[q] = 0;
+        if (q < nq) contribution<T>(sorted[i0 + q], side_out, B, k, d, U, G, coef, src[q], c[q]);
       }
 #pragma unroll
-      for (int q = 0; q < MAXC; ++q) {
-        const int cc = lane + 32 * q;
+      for (int qq = 0; qq < MAXC; ++qq) {
+        const int cc = lane + 32 * qq;
         if (cc < C) {
-          Chunk<T, EPC> x = ld_chunk<T, EPC>(src + cc * EPC);
+          Chunk<T, EPC> x[4];
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) g[q].v[e] = add_rn(g[q].v[e], side_out ? mul_rn(c, x.v[e]) : x.v[e]);
+          for (int q = 0; q < 4; ++q)
+            if (q < nq) x[q] = ld_chunk<T, EPC>(src[q] + cc * EPC);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nq) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e)
+                g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(c[q], x[q].v[e]) : x[q].v[e]);
+            }
         }
       }
     }
-    T* P = (T*)(side_out ? A.out : A.in);
-    if (!A.sparse) {
-      T* D = (T*)(side_out ? A.dense_g_out : A.dense_g_in);
 #pragma unroll
-      for (int q = 0; q < MAXC; ++q) {
-        const int cc = lane + 32 * q;
-        if (cc < C) st_chunk<T, EPC>(D + row * d + cc * EPC, g[q]);
+    for (int qq = 0; qq < MAXC; ++qq) {
+      const int cc = lane + 32 * qq;
+      if (cc < C) {
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) part[warp * d + cc * EPC + e] = g[qq].v[e];
       }
-      if (lane == 0) (side_out ? A.touched_out : A.touched_in)[row] = 1;
-      continue;
     }
+    __syncthreads();
+    T* P = (T*)(side_out ? A.out : A.in);
     T* M = (T*)(side_out ? A.m_out : A.m_in);
     T* Vv = (T*)(side_out ? A.v_out : A.v_in);
-    int32_t* steps = side_out ? A.steps_out : A.steps_in;
-    int t = 0;
-    if (lane == 0) {
-      t = steps[row] + 1;
-      steps[row] = t;
-    }
-    t = __shfl_sync(0xffffffffu, t, 0);
-    const T bc1 = (T)(1.0 - pow(0.9, (double)t));
-    const T bc2 = (T)(1.0 - pow(0.999, (double)t));
+    const T bc1 = (T)sg.bc1, bc2 = (T)sg.bc2;
     bool changed = false;
+    for (int e = threadIdx.x; e < d; e += kHeavyThreads) {
+      T gr = part[e];
 #pragma unroll
-    for (int q = 0; q < MAXC; ++q) {
-      const int cc = lane + 32 * q;
-      if (cc < C) {
-        const int64_t o = row * d + cc * EPC;
-        Chunk<T, EPC> p = ld_chunk_rw<T, EPC>(P + o);
-        Chunk<T, EPC> m = ld_chunk_rw<T, EPC>(M + o);
-        Chunk<T, EPC> vv = ld_chunk_rw<T, EPC>(Vv + o);
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) {
-          const T gr = g[q].v[e];
-          m.v[e] = add_rn(mul_rn(b1, m.v[e]), mul_rn(omb1, gr));
-          vv.v[e] = add_rn(mul_rn(b2, vv.v[e]), mul_rn(mul_rn(omb2, gr), gr));
-          const T mh = div_rn(m.v[e], bc1);
-          const T vh = div_rn(vv.v[e], bc2);
-          const T upd = div_rn(mul_rn(lr, mh), add_rn(sqrt_rn(vh), eps));
-          const T np_ = sub_rn(p.v[e], upd);
-          changed |= (np_ != p.v[e]) || (np_ != np_);
-          p.v[e] = np_;
-        }
-        st_chunk<T, EPC>(P + o, p);
-        st_chunk<T, EPC>(M + o, m);
-        st_chunk<T, EPC>(Vv + o, vv);
+      for (int w = 1; w < W; ++w) gr = add_rn(gr, part[w * d + e]);
+      const int64_t o = row * d + e;
+      if (!A.sparse) {
+        ((T*)(side_out ? A.dense_g_out : A.dense_g_in))[o] = gr;
+        continue;
       }
+      const T m = add_rn(mul_rn(b1, M[o]), mul_rn(omb1, gr));
+      const T vv = add_rn(mul_rn(b2, Vv[o]), mul_rn(mul_rn(omb2, gr), gr));
+      const T upd = div_rn(mul_rn(lr, div_rn(m, bc1)), add_rn(sqrt_rn(div_rn(vv, bc2)), eps));
+      const T p = P[o];
+      const T np_ = sub_rn(p, upd);
+      changed |= (np_ != p) || (np_ != np_);
+      P[o] = np_;
+      M[o] = m;
+      Vv[o] = vv;
     }
-    changed = __any_sync(0xffffffffu, changed);
-    if (lane == 0) {
+    changed = __syncthreads_or(changed);
+    if (threadIdx.x == 0) {
       (side_out ? A.touched_out : A.touched_in)[row] = 1;
-      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+      if (changed && A.sparse) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+      A.cnt[key] = 0;
     }
   }
 }
@@ -769,10 +1294,111 @@ static int dispatch_rows(int precision, int d, Args&&... args) {
   return -1;
 }
 
+// shared memory of the bulk gather: barriers + per-warp two-stage ring of 2+k rows
+static inline size_t bulk_smem_bytes(int d, int k, size_t es) {
+  return 128 + (size_t)kBulkWarps * 2 * (2 + k) * d * es;
+}
+static constexpr size_t kBulkSmemMax = 112 * 1024;  // two CTAs per SM
+
 template <typename T, int EPC, int MAXC>
 struct LaunchPair {
+  // register path: negatives gathered per group, as many as fit in registers
+  static constexpr int NG = MAXC <= 2 ? 5 : (MAXC <= 4 ? 2 : 1);
   static int run(const PairArgs& a, const void* in, const void* out, unsigned grid, cudaStream_t st) {
-    sgns_pair_kernel<T, EPC, MAXC><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
+    const size_t smem = bulk_smem_bytes(a.d, a.k, sizeof(T));
+    const bool bulk = (a.d * sizeof(T)) % 16 == 0 && EPC * sizeof(T) == 16 && smem <= kBulkSmemMax &&
+                      getenv("WV_SGNS_REG_GATHER") == nullptr;
+    if (bulk) {
+      static bool attr_set[16] = {false};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev >= 0 && dev < 16 && !attr_set[dev]) {
+        WV_CUDA(cudaFuncSetAttribute(sgns_gather_bulk_kernel<T, EPC, MAXC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmemMax));
+        attr_set[dev] = true;
+      }
+      const int64_t blocks = (a.B + kBulkWarps - 1) / kBulkWarps;
+      const unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+      sgns_gather_bulk_kernel<T, EPC, MAXC><<<g, kBulkThreads, smem, st>>>(a, (const T*)in, (const T*)out);
+    } else {
+      sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
+    }
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+};
+
+// side stream + fork/join events (per host thread and device) so the grouping
+// sort runs concurrently with the gather kernel; works eagerly and under
+// CUDA-graph capture (the side stream joins the capture through the events)
+struct SideStream {
+  int dev = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static cudaError_t side_stream(SideStream** out) {
+  static thread_local SideStream tab[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  SideStream& ss = tab[dev];
+  if (ss.s == nullptr) {
+    e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    ss.dev = dev;
+  }
+  *out = &ss;
+  return cudaSuccess;
+}
+
+// Workspace of one SGNS replica: the persistent per-row counters first, then
+// the per-batch buffers.  With base == nullptr only the size is computed.
+struct BatchWs {
+  uint32_t* cnt;
+  uint32_t* gctr;
+  void* U;
+  void* G;
+  void* coef;
+  int32_t* idx;
+  uint32_t* uniq;
+  uint32_t* list;
+  uint32_t* list_tmp;
+  Segment* segs;
+  Segment* heavy;
+  double* partials;
+};
+
+static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, int64_t es, BatchWs& w) {
+  const int64_t items = B * (2 + k);
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) -> void* {
+    void* p = base ? base + off : nullptr;
+    off += al256(bytes);
+    return p;
+  };
+  w.cnt = (uint32_t*)take(2 * V * 4);
+  w.gctr = (uint32_t*)take(64);
+  w.U = take(B * d * es);
+  w.G = take(B * d * es);
+  w.coef = take(B * (k + 1) * es);
+  w.idx = (int32_t*)take(items * 4);
+  w.uniq = (uint32_t*)take(items * 4);
+  w.list = (uint32_t*)take(items * 4);
+  w.list_tmp = (uint32_t*)take(items * 4);
+  w.segs = (Segment*)take(items * (int64_t)sizeof(Segment));
+  w.heavy = (Segment*)take((items / (kLightMax + 1) + 1) * (int64_t)sizeof(Segment));
+  w.partials = (double*)take(148 * 32 * 8);
+  return off + 1024;
+}
+
+template <typename T, int EPC, int MAXC>
+struct LaunchHeavy {
+  static int run(const OwnerArgs& a, unsigned grid, cudaStream_t st) {
+    sgns_heavy_kernel<T, EPC, MAXC><<<grid, kHeavyThreads, (kHeavyThreads / 32) * a.d * sizeof(T), st>>>(a);
     WV_LAUNCH_CHECK();
     return 0;
   }
@@ -963,23 +1589,33 @@ int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, voi
 int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
                                       int precision) {
   using namespace wv;
-  const int64_t es = precision == WV_FP64 ? 8 : 4;
-  const int64_t items = batch * (2 + negatives);
-  const int bits = bits_for((uint64_t)(2 * vocab_size - 1));
-  return al256(batch * vector_size * es) * 2 + al256(batch * (negatives + 1) * es) + al256(items * 4) * 2 +
-         al256(radix_ws_bytes(items, bits)) + al256(items * 8) + al256(148 * 32 * 8) + al256(64) + 1024;
+  BatchWs bw;
+  return carve_batch_ws(nullptr, vocab_size, vector_size, negatives, batch, precision == WV_FP64 ? 8 : 4, bw);
 }
 
-// One SGNS batch: pair phase -> stable grouping sort -> owner Adam phase.
+// Zero the workspace's persistent per-row counters; required once after the
+// workspace is allocated (every batch leaves them zero again).
+int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size, int negatives,
+                           int64_t batch, int precision, void* stream) {
+  using namespace wv;
+  BatchWs bw;
+  const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, negatives, batch,
+                                      precision == WV_FP64 ? 8 : 4, bw);
+  WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
+  WV_CUDA(cudaMemsetAsync(bw.cnt, 0, 2 * vocab_size * 4, (cudaStream_t)stream));
+  return 0;
+}
+
+// One SGNS batch: decode -> (gather || grouping) -> owner Adam phase.
 // Every launch is stream-ordered and reads the batch cursor from `state`, so
 // the sequence is CUDA-graph capturable and replayable.
 int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream) {
   return wv_sgns_batch_phases(model, batch, ws, ws_bytes, WV_PHASE_ALL, stream);
 }
 
-// The batch split into its three phases (pair gather / grouping sort /
-// owner update) so callers can bracket each with events; all state flows
-// through the workspace, so calling the phases in order equals one batch.
+// The batch split into its phases (PAIRS = decode + gather, GROUP = row
+// grouping, UPDATE = owner Adam) so callers can run them separately; all state
+// flows through the workspace, so calling the phases in order equals one batch.
 int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int phases,
                          void* stream) {
   using namespace wv;
@@ -988,32 +1624,25 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   const int k = batch->negatives;
   const int64_t B = batch->batch_rows;
   WV_CHECK_ARG(B >= 1, "empty batch");
-  WV_CHECK_ARG(2 * V < (int64_t)0xffffffffLL, "vocabulary too large for 32-bit sort keys");
+  WV_CHECK_ARG(k >= 0 && k <= 30, "negative_samples must be in [0, 30]");
+  WV_CHECK_ARG(2 * V < (int64_t)0xffffffffLL, "vocabulary too large for 32-bit row keys");
   WV_CHECK_ARG(B * (2 + k) < (int64_t)0xffffffffLL, "batch too large");
-  WV_CHECK_ARG(ws_bytes >= wv_sgns_batch_workspace_bytes(V, d, k, B, model->precision), "workspace too small");
   WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t es = model->precision == WV_FP64 ? 8 : 4;
   const int64_t items = B * (2 + k);
-  const int bits = bits_for((uint64_t)(2 * V - 1));
-  char* w = (char*)ws;
-  void* U = w;
-  w += al256(B * d * es);
-  void* G = w;
-  w += al256(B * d * es);
-  void* coef = w;
-  w += al256(B * (k + 1) * es);
-  uint32_t* keys = (uint32_t*)w;
-  w += al256(items * 4);
-  uint32_t* vals = (uint32_t*)w;
-  w += al256(items * 4);
-  void* rws = w;
-  w += al256(radix_ws_bytes(items, bits));
-  int64_t* seg_start = (int64_t*)w;
-  w += al256(items * 8);
-  double* partials = (double*)w;
-  w += al256(148 * 32 * 8);
-  uint32_t* seg_count = (uint32_t*)w;
+  BatchWs bw;
+  const int64_t need = carve_batch_ws((char*)ws, V, d, k, B, es, bw);
+  WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
+  void* U = bw.U;
+  void* G = bw.G;
+  void* coef = bw.coef;
+  int32_t* idx = bw.idx;
+  Segment* segs = bw.segs;
+  Segment* heavy = bw.heavy;
+  double* partials = bw.partials;
+  uint32_t* gctr = bw.gctr;
+  uint32_t* seg_count = gctr + GC_LIGHT;
 
   PairArgs pa;
   pa.mode = batch->mode;
@@ -1039,23 +1668,59 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   pa.U = U;
   pa.G = G;
   pa.coef = coef;
-  pa.keys = keys;
-  pa.vals = vals;
+  pa.cnt = bw.cnt;
+  pa.uniq = bw.uniq;
+  pa.gctr = gctr;
+  pa.idx = idx;
   pa.partials = partials;
   pa.state = model->state;
-  pa.seg_count = seg_count;
   const unsigned pgrid = grid_for(B, kPairWarps, 148 * 32);
   int rc = 0;
+  // PAIRS = decode + gather; GROUP = the grouping sort.  When both are asked
+  // for, the sort runs on a side stream concurrently with the gather.
+  const bool overlap = (phases & WV_PHASE_PAIRS) && (phases & WV_PHASE_GROUP);
+  // optional timestamps (bench/profiling): slots base+0..6 = batch start, decode
+  // end, gather end, join, owner end, sort start, sort end
+  void* timer = batch->timer;
+  const int tb = (int)batch->timer_base;
+#define WV_STAMP(slot, strm) \
+  if (timer) WV_CUDA_RC(wv_timer_record(timer, tb + (slot), (void*)(strm)))
+  WV_STAMP(0, st);
+  if (phases & WV_PHASE_PAIRS) {
+    WV_CUDA(cudaMemsetAsync(gctr, 0, 4 * sizeof(uint32_t), st));
+    sgns_decode_kernel<<<grid_for(B, 256, 148 * 16), 256, 0, st>>>(pa);
+    WV_LAUNCH_CHECK();
+  }
+  WV_STAMP(1, st);
+  SideStream* side = nullptr;
+  cudaStream_t sort_st = st;
+  if (overlap) {
+    WV_CUDA(side_stream(&side));
+    WV_CUDA(cudaEventRecord(side->fork, st));
+    WV_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+    sort_st = side->s;
+  }
+  if (phases & WV_PHASE_GROUP) {
+    WV_STAMP(5, sort_st);
+    group_segments<<<grid_for(items, 256, 148 * 8), 256, 0, sort_st>>>(bw.uniq, bw.cnt, gctr, V, model->sparse,
+                                                                       model->steps_in, model->steps_out, segs,
+                                                                       heavy, items);
+    WV_LAUNCH_CHECK();
+    group_place<<<grid_for(items, 256, 148 * 8), 256, 0, sort_st>>>(idx, B, k, V, bw.cnt, bw.list);
+    WV_LAUNCH_CHECK();
+    WV_STAMP(6, sort_st);
+  }
   if (phases & WV_PHASE_PAIRS) {
     rc = dispatch_rows<LaunchPair>(model->precision, d, pa, (const void*)model->input, (const void*)model->output,
                                    pgrid, st);
     if (rc) return rc;
   }
-  if (phases & WV_PHASE_GROUP) {
-    WV_CUDA(radix_sort_pairs(keys, vals, items, bits, rws, st));
-    seg_heads<<<grid_for(items, 256), 256, 0, st>>>(keys, items, seg_start, seg_count, model->state, B);
-    WV_LAUNCH_CHECK();
+  WV_STAMP(2, st);
+  if (overlap) {
+    WV_CUDA(cudaEventRecord(side->join, side->s));
+    WV_CUDA(cudaStreamWaitEvent(st, side->join, 0));
   }
+  WV_STAMP(3, st);
   if (!(phases & WV_PHASE_UPDATE)) return 0;
   OwnerArgs oa;
   oa.V = V;
@@ -1063,9 +1728,12 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.k = k;
   oa.B = B;
   oa.n_items = items;
-  oa.keys = keys;
-  oa.vals = vals;
-  oa.seg_start = seg_start;
+  oa.list = bw.list;
+  oa.list_tmp = bw.list_tmp;
+  oa.cnt = bw.cnt;
+  oa.slot_bits = bits_for((uint64_t)(items - 1));
+  oa.segs = segs;
+  oa.heavy = heavy;
   oa.seg_count = seg_count;
   oa.U = U;
   oa.G = G;
@@ -1076,8 +1744,6 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.v_in = model->v_in;
   oa.m_out = model->m_out;
   oa.v_out = model->v_out;
-  oa.steps_in = model->steps_in;
-  oa.steps_out = model->steps_out;
   oa.touched_in = model->touched_in;
   oa.touched_out = model->touched_out;
   oa.modified_in = model->modified_in;
@@ -1087,9 +1753,13 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.dense_g_in = model->dense_g_in;
   oa.dense_g_out = model->dense_g_out;
   oa.state = model->state;
-  const unsigned ogrid = grid_for(items, kOwnerThreads / 32, 148 * 16);
+  const unsigned ogrid = grid_for(items * ((d + 127) / 128), kOwnerThreads / 32, 148 * 32);
+  rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 4), st);
+  if (rc) return rc;
   rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, ogrid, st);
   if (rc) return rc;
+  WV_STAMP(4, st);
+#undef WV_STAMP
   if (!model->sparse) {
     const int64_t n = V * (int64_t)d;
     if (model->precision == WV_FP32) {

@@ -41,6 +41,9 @@ CBOW = "cbow"
 DEFAULT_MEMORY_BUDGET = 1 << 30
 MEMORY_BUDGET_ENV = "WALKVEC_MEMORY_BUDGET"
 REPRODUCIBLE_SYNC_BATCHES = 64
+# device timestamps per profiled batch (WvSgnsBatch.timer): start, decode end,
+# gather end, join, owner end, sort start, sort end
+STAMPS_PER_BATCH = 7
 
 
 class TrainingDiverged(RuntimeError):
@@ -365,12 +368,14 @@ class _Replica:
         self.ws = torch.empty(_lib.query("wv_sgns_batch_workspace_bytes", params.V, params.d, trainer.k,
                                          trainer.batch_size, params.precision), dtype=torch.uint8,
                               device=trainer.dev)
+        _lib.call("wv_sgns_workspace_init", _lib.ptr(self.ws), self.ws.numel(), params.V, params.d, trainer.k,
+                  trainer.batch_size, params.precision, _lib.stream_ptr())
         self.graphs = {}
-        self.graph_events = {}  # key -> DeviceTimer of 4 events per batch, last replay (profiling)
+        self.graph_events = {}  # key -> DeviceTimer, STAMPS_PER_BATCH per batch, last replay (profiling)
         self.graph_launches = {}  # key -> kernels per replay
 
     def launch(self, rows: int, events=None):
-        """One batch; ``events`` = (DeviceTimer, first slot): 4 stamps around the three phases."""
+        """One batch; ``events`` = (DeviceTimer, first slot): STAMPS_PER_BATCH device timestamps."""
         t = self.t
         bs = t.batch_struct
         bs.batch_rows = int(rows)
@@ -379,11 +384,12 @@ class _Replica:
                       _lib.stream_ptr())
             return
         timer, base = events
-        timer.record(base)
-        for i, ph in enumerate((_lib.PHASE_PAIRS, _lib.PHASE_GROUP, _lib.PHASE_UPDATE)):
-            _lib.call("wv_sgns_batch_phases", C.byref(self.p.struct), C.byref(bs), _lib.ptr(self.ws),
-                      self.ws.numel(), ph, _lib.stream_ptr())
-            timer.record(base + i + 1)
+        bs.timer, bs.timer_base = timer.h, int(base)
+        try:
+            _lib.call("wv_sgns_batch", C.byref(self.p.struct), C.byref(bs), _lib.ptr(self.ws), self.ws.numel(),
+                      _lib.stream_ptr())
+        finally:
+            bs.timer, bs.timer_base = None, 0
 
     def run(self, count: int, rows: int):
         """``count`` consecutive batches of ``rows`` pairs, CUDA-graph replayed."""
@@ -401,11 +407,11 @@ class _Replica:
             g = torch.cuda.CUDAGraph()
             evs = None
             if self.t.profile:
-                evs = _lib.DeviceTimer(4 * key[1])
+                evs = _lib.DeviceTimer(STAMPS_PER_BATCH * key[1])
             before = _lib.launch_count()
             with torch.cuda.graph(g):
                 for i in range(key[1]):
-                    self.launch(rows, None if evs is None else (evs, 4 * i))
+                    self.launch(rows, None if evs is None else (evs, STAMPS_PER_BATCH * i))
             self.graphs[key] = g
             self.graph_events[key] = evs
             self.graph_launches[key] = _lib.launch_count() - before
