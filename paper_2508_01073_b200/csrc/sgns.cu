@@ -111,6 +111,37 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Eight warp sums at once: a transposed butterfly (offsets 16, 8, 4 halve the
+// value set, 2 and 1 finish) -- 9 shuffles instead of 40, and every value sees
+// exactly the pairwise-add tree of warp_sum.  Lane l returns value (l >> 2) & 7.
+template <typename T>
+__device__ __forceinline__ T warp_sum8(const T (&p)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  T a[4], b2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const T keep = h16 ? p[4 + i] : p[i];
+    const T send = h16 ? p[i] : p[4 + i];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const T keep = h8 ? a[2 + i] : a[i];
+    const T send = h8 ? a[i] : a[2 + i];
+    b2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  T c;
+  {
+    const T keep = h4 ? b2[1] : b2[0];
+    const T send = h4 ? b2[0] : b2[1];
+    c = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  c += __shfl_xor_sync(0xffffffffu, c, 1);
+  return c;
+}
+
 // numpy logaddexp(0, x)
 __device__ __forceinline__ double log1pexp(double x) { return x > 0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
 
@@ -238,68 +269,69 @@ __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
   if (atomicAdd(A.cnt + key, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = key;
 }
 
-// Phase 1a, thread per pair: the batch's row indices (centre, context, k
-// negatives) and the grouping-sort input.  Pair decode (Feistel position ->
-// length class -> walk -> window slot) is a chain of dependent L2 reads, so
-// it runs here with one thread per pair (latency hidden by parallelism)
-// instead of serialising inside the gather warps.
-__global__ void __launch_bounds__(256) sgns_decode_kernel(PairArgs A) {
+// Phase 1a, thread per item: the batch's row indices (centre, context, k
+// negatives) and the row claims for grouping.  Item j = 0 decodes the pair
+// (Feistel position -> length class -> walk -> window slot: a chain of
+// dependent L2 reads) and writes centre and context; items j >= 2 draw one
+// negative each.  Thread-per-item spreads the latency chains over all SMs.
+__global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
   const int k = A.k;
+  const int R = 2 + k;
   const int64_t B = A.B;
+  const int64_t items = B * R;
   const int64_t lo = A.state->lo;
   const uint64_t epoch = (uint64_t)A.state->epoch;
   Feistel fs;
   if (A.mode == WV_PAIRS_NATIVE) fs = make_feistel(A.seed, epoch, A.N);
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = it / R;
+    const int jj = (int)(it - b * R);
     const int64_t pos = lo + b;
-    int32_t center, context;
-    if (A.mode == WV_PAIRS_NATIVE) {
-      const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, A.N);
-      int lo_c = 0, hi_c = A.n_classes;  // last class with start <= q
-      while (hi_c - lo_c > 1) {
-        int mid = (lo_c + hi_c) >> 1;
-        if (A.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
+    int32_t* row = A.idx + b * R;
+    if (jj == 0) {
+      int32_t center, context;
+      if (A.mode == WV_PAIRS_NATIVE) {
+        const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, A.N);
+        int lo_c = 0, hi_c = A.n_classes;  // last class with start <= q
+        while (hi_c - lo_c > 1) {
+          int mid = (lo_c + hi_c) >> 1;
+          if (A.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
+        }
+        const int64_t L = A.class_len[lo_c];
+        const int64_t np = walk_pairs(L, A.window);
+        const int64_t r = q - A.class_pair_start[lo_c];
+        const int64_t wslot = r / np;
+        const int64_t local = r - wslot * np;
+        const int64_t walk = A.walks_by_class[A.class_walk_start[lo_c] + wslot];
+        int64_t cpos, xpos;
+        walk_pair_pos(L, A.window, local, cpos, xpos);
+        const int64_t base = A.offsets[walk];
+        center = A.tokens[base + cpos];
+        context = A.tokens[base + xpos];
+      } else {
+        const int64_t pi = A.perm[pos];
+        center = A.pairs[2 * pi];
+        context = A.pairs[2 * pi + 1];
       }
-      const int64_t L = A.class_len[lo_c];
-      const int64_t np = walk_pairs(L, A.window);
-      const int64_t r = q - A.class_pair_start[lo_c];
-      const int64_t wslot = r / np;
-      const int64_t local = r - wslot * np;
-      const int64_t walk = A.walks_by_class[A.class_walk_start[lo_c] + wslot];
-      int64_t cpos, xpos;
-      walk_pair_pos(L, A.window, local, cpos, xpos);
-      const int64_t base = A.offsets[walk];
-      center = A.tokens[base + cpos];
-      context = A.tokens[base + xpos];
-    } else {
-      const int64_t pi = A.perm[pos];
-      center = A.pairs[2 * pi];
-      context = A.pairs[2 * pi + 1];
-    }
-    int32_t* row = A.idx + b * (2 + k);
-    row[0] = center;
-    row[1] = context;
-    group_claim(A, (uint32_t)center);
-    group_claim(A, (uint32_t)(context + A.V));
-    // native negatives: Philox4x32 counter (position, epoch, call), two draws per call
-    uint32_t rnd[4];
-    for (int j = 0; j < k; ++j) {
+      row[0] = center;
+      row[1] = context;
+      group_claim(A, (uint32_t)center);
+      group_claim(A, (uint32_t)(context + A.V));
+    } else if (jj >= 2) {
+      const int j = jj - 2;
       int32_t neg;
       if (A.mode == WV_PAIRS_NATIVE) {
-        if ((j & 1) == 0) {
-          rnd[0] = (uint32_t)pos;
-          rnd[1] = (uint32_t)((uint64_t)pos >> 32);
-          rnd[2] = (uint32_t)epoch;
-          rnd[3] = (uint32_t)(j >> 1);
-          philox4x32_10(rnd, (uint32_t)A.seed ^ 0xA5A5F00Du, (uint32_t)(A.seed >> 32) ^ 0x3C6EF372u);
-        }
+        // Philox4x32 counter (position, epoch, j/2): two draws per call
+        uint32_t rnd[4] = {(uint32_t)pos, (uint32_t)((uint64_t)pos >> 32), (uint32_t)epoch, (uint32_t)(j >> 1)};
+        philox4x32_10(rnd, (uint32_t)A.seed ^ 0xA5A5F00Du, (uint32_t)(A.seed >> 32) ^ 0x3C6EF372u);
         const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
         const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)A.n_candidates);
         neg = A.candidates ? A.candidates[ci] : (int32_t)ci;
       } else {
         neg = A.negatives[pos * k + j];
       }
-      row[2 + j] = neg;
+      row[jj] = neg;
       group_claim(A, (uint32_t)(neg + A.V));
     }
   }
@@ -434,22 +466,30 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
       const int c = lane + 32 * q;
       if (c < C) u[q] = *reinterpret_cast<const Chunk<T, EPC>*>(rows + c * EPC);
     }
-    // dot j = <u, row 1+j> (j = 0: context, j >= 1: negative j-1); lane j keeps dot j
+    // dot j = <u, row 1+j> (j = 0: context, j >= 1: negative j-1), eight at a
+    // time through one transposed butterfly; lane j ends up holding dot j
     T mydot = 0;
-    for (int j = 0; j <= k; ++j) {
-      const T* rj = rows + (size_t)(1 + j) * d;
-      T dot = 0;
+    for (int j0 = 0; j0 <= k; j0 += 8) {
+      T part[8];
 #pragma unroll
-      for (int q = 0; q < MAXC; ++q) {
-        const int c = lane + 32 * q;
-        if (c < C) {
-          const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rj + c * EPC);
+      for (int t = 0; t < 8; ++t) {
+        part[t] = 0;
+        if (j0 + t <= k) {
+          const T* rj = rows + (size_t)(1 + j0 + t) * d;
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) dot += u[q].v[e] * x.v[e];
+          for (int q = 0; q < MAXC; ++q) {
+            const int c = lane + 32 * q;
+            if (c < C) {
+              const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rj + c * EPC);
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) part[t] += u[q].v[e] * x.v[e];
+            }
+          }
         }
       }
-      dot = warp_sum(dot);
-      if (lane == j) mydot = dot;
+      const T red = warp_sum8(part);  // dot j0 + ((lane >> 2) & 7)
+      const T got = __shfl_sync(0xffffffffu, red, (lane & 7) << 2);
+      if (lane >= j0 && lane < j0 + 8) mydot = got;
     }
     // lane j: loss term and coefficient of dot j
     T mycoef = 0;
@@ -659,6 +699,7 @@ __global__ void __launch_bounds__(kPairThreads) sgns_gather_kernel(PairArgs A, c
 // entities) go to the CTA-per-row kernel; the rest to the warp-per-row one.
 constexpr int kLightMax = 16;
 constexpr int kHeavyThreads = 256;
+constexpr int kRankSortMax = 1024;  // heavy rows up to this many slots sort in shared memory
 
 // One record per unique (matrix, row) of the batch, built by group_segments.
 struct Segment {
@@ -772,6 +813,29 @@ struct OwnerArgs {
   WvSgnsDevState* state;
 };
 
+// RowAdam element update (w2v.py:384-395): m, v recurrences, bias-corrected
+// step.  float64 keeps numpy's exact operation order (correctly rounded
+// divisions); the float32 store multiplies by the per-row reciprocals of the
+// bias corrections and uses a fast divide (a few ulp; the fp32 store is
+// tolerance-checked against the reference, not bit-checked).
+template <typename T>
+__device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, double bc1, double bc2, T lr) {
+  const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
+  m = add_rn(mul_rn(b1, m), mul_rn(omb1, g));
+  v = add_rn(mul_rn(b2, v), mul_rn(mul_rn(omb2, g), g));
+  T upd;
+  if constexpr (sizeof(T) == 8) {
+    upd = div_rn(mul_rn(lr, div_rn(m, (T)bc1)), add_rn(sqrt_rn(div_rn(v, (T)bc2)), eps));
+  } else {
+    const float mh = m * (float)(1.0 / bc1), vh = v * (float)(1.0 / bc2);
+    upd = __fdividef(lr * mh, __fsqrt_rn(vh) + eps);
+  }
+  const T np_ = sub_rn(p, upd);
+  const T old = p;
+  p = np_;
+  return (np_ != old) || (np_ != np_) ? T(1) : T(0);
+}
+
 // Sorted contribution value v -> (source row, coefficient): input-matrix rows
 // take the pair's centre gradient row G[b] (coefficient 1); output-matrix rows
 // take coef * U[b] (the context's gpos or negative j's gneg).
@@ -783,17 +847,18 @@ __device__ __forceinline__ void contribution(uint32_t v, bool side_out, int64_t 
     c = 1;
     return;
   }
-  const int64_t s = (int64_t)v - B;
-  int64_t pp, j;
-  if (s < B) {
+  const uint32_t s = v - (uint32_t)B;
+  uint32_t pp, j;
+  if (s < (uint32_t)B) {
     pp = s;
     j = 0;
   } else {
-    pp = (s - B) / k;
-    j = 1 + (s - B) - pp * k;
+    const uint32_t t = s - (uint32_t)B;
+    pp = t / (uint32_t)k;
+    j = 1 + t - pp * (uint32_t)k;
   }
-  src = U + pp * d;
-  c = __ldg(coef + pp * (k + 1) + j);
+  src = U + (int64_t)pp * d;
+  c = __ldg(coef + (int64_t)pp * (k + 1) + j);
 }
 
 // Phase 3: one warp per (unique row, 32-chunk slice of the row): sum the row's
@@ -813,7 +878,7 @@ __global__ void __launch_bounds__(kOwnerThreads, 4) sgns_owner_kernel(OwnerArgs 
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // the batch is consumed: advance the cursor (read by the next batch's decode)
     WvSgnsDevState* st = A.state;
-    st->rows_updated += nseg;
+    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)nseg);
     st->lo += B;
     st->batch += 1;
     st->step += 1;
@@ -884,21 +949,10 @@ __global__ void __launch_bounds__(kOwnerThreads, 4) sgns_owner_kernel(OwnerArgs 
       }
       continue;
     }
-    const T bc1 = (T)sg.bc1, bc2 = (T)sg.bc2;
     bool changed = false;
     if (active) {
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) {
-        const T gr = g.v[e];
-        m.v[e] = add_rn(mul_rn(b1, m.v[e]), mul_rn(omb1, gr));
-        vv.v[e] = add_rn(mul_rn(b2, vv.v[e]), mul_rn(mul_rn(omb2, gr), gr));
-        const T mh = div_rn(m.v[e], bc1);
-        const T vh = div_rn(vv.v[e], bc2);
-        const T upd = div_rn(mul_rn(lr, mh), add_rn(sqrt_rn(vh), eps));
-        const T np_ = sub_rn(p.v[e], upd);
-        changed |= (np_ != p.v[e]) || (np_ != np_);
-        p.v[e] = np_;
-      }
+      for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], sg.bc1, sg.bc2, lr) != T(0);
       st_chunk<T, EPC>(P + o, p);
       st_chunk<T, EPC>(M + o, m);
       st_chunk<T, EPC>(Vv + o, vv);
@@ -987,6 +1041,7 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
   extern __shared__ unsigned char smem_raw[];
   T* part = reinterpret_cast<T*>(smem_raw);  // [W][d]
   __shared__ uint32_t sort_hist[kHeavyThreads / 32][256];
+  __shared__ uint32_t rank_in[kRankSortMax], rank_out[kRankSortMax];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = A.d, k = A.k;
   const int C = d / EPC;
@@ -997,7 +1052,8 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
   const T* coef = (const T*)A.coef;
   const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
   const T lr = (T)A.lr;
-  if (blockIdx.x == 0 && threadIdx.x == 0) A.state->rows_updated += nh;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd((unsigned long long*)&A.state->rows_updated, (unsigned long long)nh);
   for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
     const Segment sg = A.heavy[h];
     const uint32_t key = sg.key;
@@ -1005,8 +1061,23 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
     const int64_t row = side_out ? (int64_t)key - A.V : (int64_t)key;
     // restore slot order of the row's list (stable LSD radix sort, ping-pong
     // with the scratch list at the same offsets)
-    const uint32_t* sorted = cta_sort_slots(const_cast<uint32_t*>(A.list) + sg.start, A.list_tmp + sg.start, sg.len,
-                                            A.slot_bits, sort_hist);
+    const uint32_t* sorted;
+    if (sg.len <= (uint32_t)kRankSortMax) {
+      // rank sort in shared memory: out[#smaller] = x (slots are distinct)
+      for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads) rank_in[i] = A.list[sg.start + i];
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads) {
+        const uint32_t x = rank_in[i];
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < sg.len; ++j) r += rank_in[j] < x;
+        rank_out[r] = x;
+      }
+      __syncthreads();
+      sorted = rank_out;
+    } else {
+      sorted = cta_sort_slots(const_cast<uint32_t*>(A.list) + sg.start, A.list_tmp + sg.start, sg.len, A.slot_bits,
+                              sort_hist);
+    }
     const uint32_t per = (sg.len + W - 1) / W;
     const uint32_t lo = min(sg.len, per * warp), hi = min(sg.len, per * (warp + 1));
     Chunk<T, EPC> g[MAXC];
@@ -1054,7 +1125,6 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
     T* P = (T*)(side_out ? A.out : A.in);
     T* M = (T*)(side_out ? A.m_out : A.m_in);
     T* Vv = (T*)(side_out ? A.v_out : A.v_in);
-    const T bc1 = (T)sg.bc1, bc2 = (T)sg.bc2;
     bool changed = false;
     for (int e = threadIdx.x; e < d; e += kHeavyThreads) {
       T gr = part[e];
@@ -1065,13 +1135,9 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
         ((T*)(side_out ? A.dense_g_out : A.dense_g_in))[o] = gr;
         continue;
       }
-      const T m = add_rn(mul_rn(b1, M[o]), mul_rn(omb1, gr));
-      const T vv = add_rn(mul_rn(b2, Vv[o]), mul_rn(mul_rn(omb2, gr), gr));
-      const T upd = div_rn(mul_rn(lr, div_rn(m, bc1)), add_rn(sqrt_rn(div_rn(vv, bc2)), eps));
-      const T p = P[o];
-      const T np_ = sub_rn(p, upd);
-      changed |= (np_ != p) || (np_ != np_);
-      P[o] = np_;
+      T p = P[o], m = M[o], vv = Vv[o];
+      changed |= adam_elem<T>(p, m, vv, gr, sg.bc1, sg.bc2, lr) != T(0);
+      P[o] = p;
       M[o] = m;
       Vv[o] = vv;
     }
@@ -1081,6 +1147,7 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
       if (changed && A.sparse) (side_out ? A.modified_out : A.modified_in)[row] = 1;
       A.cnt[key] = 0;
     }
+    __syncthreads();  // shared buffers are reused by the next heavy row
   }
 }
 
@@ -1688,7 +1755,7 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   WV_STAMP(0, st);
   if (phases & WV_PHASE_PAIRS) {
     WV_CUDA(cudaMemsetAsync(gctr, 0, 4 * sizeof(uint32_t), st));
-    sgns_decode_kernel<<<grid_for(B, 256, 148 * 16), 256, 0, st>>>(pa);
+    sgns_decode_kernel<<<grid_for(items, 128, 148 * 32), 128, 0, st>>>(pa);
     WV_LAUNCH_CHECK();
   }
   WV_STAMP(1, st);
@@ -1754,10 +1821,16 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.dense_g_out = model->dense_g_out;
   oa.state = model->state;
   const unsigned ogrid = grid_for(items * ((d + 127) / 128), kOwnerThreads / 32, 148 * 32);
-  rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 4), st);
+  // heavy rows (side stream) and light rows (main stream) are disjoint: run both at once
+  if (side == nullptr) WV_CUDA(side_stream(&side));
+  WV_CUDA(cudaEventRecord(side->fork, st));
+  WV_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+  rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 2), side->s);
   if (rc) return rc;
   rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, ogrid, st);
   if (rc) return rc;
+  WV_CUDA(cudaEventRecord(side->join, side->s));
+  WV_CUDA(cudaStreamWaitEvent(st, side->join, 0));
   WV_STAMP(4, st);
 #undef WV_STAMP
   if (!model->sparse) {
