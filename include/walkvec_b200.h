@@ -215,6 +215,11 @@ int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, ui
 int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, void* stream);
 int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
                                       int precision);
+/* copy the corpus side of `batch` (pair source, negatives) into the workspace;
+ * needed before replaying a CUDA graph of wv_sgns_batch calls on a new corpus
+ * (uncaptured wv_sgns_batch calls bind by themselves) */
+int wv_sgns_bind(const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size,
+                 int precision, void* stream);
 /* zero the workspace's persistent per-row counters: once after allocating it */
 int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size, int negatives,
                            int64_t batch, int precision, void* stream);

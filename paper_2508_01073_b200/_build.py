@@ -33,19 +33,24 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > mtime for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile the library (``out``/``defines``: A/B variants, loaded with WV_LIB=path)."""
+    lib = Path(out) if out else LIB
+    if not force and out is None and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB) + ".tmp"]
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-o", str(lib) + ".tmp"]
     cmd += [str(CSRC / s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    # python _build.py [-v] [--out path -DNAME=VAL ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else None
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    print(build(force=True, verbose="-v" in argv, out=out, defines=defs))

@@ -8,11 +8,13 @@ call without a CUDA device raises ``BackendUnavailable``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libwalkvec_b200.so"
+# WV_LIB overrides the in-tree library (A/B builds of kernel variants)
+LIB_PATH = Path(os.environ["WV_LIB"]) if os.environ.get("WV_LIB") else _PKG / "libwalkvec_b200.so"
 
 RNG_PCG64 = 0
 RNG_PHILOX = 1
@@ -148,6 +150,7 @@ SIGNATURES = {
     "wv_sgns_epoch_begin": (I32, [P, I64, I64, P]),
     "wv_sgns_batch_workspace_bytes": (I64, [I64, I32, I32, I64, I32]),
     "wv_sgns_workspace_init": (I32, [P, I64, I64, I32, I32, I64, I32, P]),
+    "wv_sgns_bind": (I32, [P, P, I64, I64, I32, I32, P]),
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
     "wv_replica_delta": (I32, [P, P, I64, I32, P, P]),

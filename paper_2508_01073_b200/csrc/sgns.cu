@@ -30,6 +30,13 @@ namespace wv {
 constexpr int kPairThreads = 256;
 constexpr int kPairWarps = kPairThreads / 32;
 constexpr int kOwnerThreads = 256;
+#ifndef WV_OWNER_GROUP
+#define WV_OWNER_GROUP 2
+#endif
+#ifndef WV_OWNER_MINB
+#define WV_OWNER_MINB 4
+#endif
+constexpr int kOwnerGroup = WV_OWNER_GROUP;  // contributions loaded together per light row
 
 // ---------------------------------------------------- precise arithmetic --
 // Explicit rounding so the update mirrors numpy's operation order (no FMA
@@ -214,14 +221,15 @@ __device__ __forceinline__ void walk_pair_pos(int64_t L, int W, int64_t q, int64
 }
 
 // ------------------------------------------------------------ the batch ---
-struct PairArgs {
+// The corpus side of a batch (pair source, negatives).  It lives in device
+// memory (the workspace) so a captured CUDA graph of batches stays valid when
+// the session moves on to the next corpus: wv_sgns_bind rewrites it.
+struct CorpusDesc {
   int mode;  // WV_PAIRS_NATIVE or WV_PAIRS_EXPLICIT
-  int64_t V;
-  int d;
-  int k;
   int window;
-  int64_t B;       // rows in this batch
-  int64_t N;       // pairs per epoch
+  int n_classes;
+  int pad;
+  int64_t N;  // pairs per epoch
   uint64_t seed;
   // native corpus index
   const int32_t* tokens;
@@ -229,14 +237,21 @@ struct PairArgs {
   const int64_t* class_len;
   const int64_t* class_pair_start;  // n_classes + 1
   const int64_t* class_walk_start;
-  int n_classes;
   const int32_t* walks_by_class;
   const int32_t* candidates;  // null => identity over [0, n_candidates)
   int64_t n_candidates;
   // explicit replay
-  const int32_t* pairs;  // [N,2]
-  const int64_t* perm;   // [N] epoch permutation
+  const int32_t* pairs;      // [N,2]
+  const int64_t* perm;       // [N] epoch permutation
   const int32_t* negatives;  // [N,k] per permuted position
+};
+
+struct PairArgs {
+  int64_t V;
+  int d;
+  int k;
+  int64_t B;  // rows in this batch
+  const CorpusDesc* desc;
   // outputs
   void* U;
   void* G;
@@ -275,6 +290,9 @@ __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
 // dependent L2 reads) and writes centre and context; items j >= 2 draw one
 // negative each.  Thread-per-item spreads the latency chains over all SMs.
 __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
+  __shared__ CorpusDesc D;
+  if (threadIdx.x == 0) D = *A.desc;
+  __syncthreads();
   const int k = A.k;
   const int R = 2 + k;
   const int64_t B = A.B;
@@ -282,7 +300,7 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
   const int64_t lo = A.state->lo;
   const uint64_t epoch = (uint64_t)A.state->epoch;
   Feistel fs;
-  if (A.mode == WV_PAIRS_NATIVE) fs = make_feistel(A.seed, epoch, A.N);
+  if (D.mode == WV_PAIRS_NATIVE) fs = make_feistel(D.seed, epoch, D.N);
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
        it += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = it / R;
@@ -291,28 +309,28 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
     int32_t* row = A.idx + b * R;
     if (jj == 0) {
       int32_t center, context;
-      if (A.mode == WV_PAIRS_NATIVE) {
-        const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, A.N);
-        int lo_c = 0, hi_c = A.n_classes;  // last class with start <= q
+      if (D.mode == WV_PAIRS_NATIVE) {
+        const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, D.N);
+        int lo_c = 0, hi_c = D.n_classes;  // last class with start <= q
         while (hi_c - lo_c > 1) {
           int mid = (lo_c + hi_c) >> 1;
-          if (A.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
+          if (D.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
         }
-        const int64_t L = A.class_len[lo_c];
-        const int64_t np = walk_pairs(L, A.window);
-        const int64_t r = q - A.class_pair_start[lo_c];
+        const int64_t L = D.class_len[lo_c];
+        const int64_t np = walk_pairs(L, D.window);
+        const int64_t r = q - D.class_pair_start[lo_c];
         const int64_t wslot = r / np;
         const int64_t local = r - wslot * np;
-        const int64_t walk = A.walks_by_class[A.class_walk_start[lo_c] + wslot];
+        const int64_t walk = D.walks_by_class[D.class_walk_start[lo_c] + wslot];
         int64_t cpos, xpos;
-        walk_pair_pos(L, A.window, local, cpos, xpos);
-        const int64_t base = A.offsets[walk];
-        center = A.tokens[base + cpos];
-        context = A.tokens[base + xpos];
+        walk_pair_pos(L, D.window, local, cpos, xpos);
+        const int64_t base = D.offsets[walk];
+        center = D.tokens[base + cpos];
+        context = D.tokens[base + xpos];
       } else {
-        const int64_t pi = A.perm[pos];
-        center = A.pairs[2 * pi];
-        context = A.pairs[2 * pi + 1];
+        const int64_t pi = D.perm[pos];
+        center = D.pairs[2 * pi];
+        context = D.pairs[2 * pi + 1];
       }
       row[0] = center;
       row[1] = context;
@@ -321,15 +339,15 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
     } else if (jj >= 2) {
       const int j = jj - 2;
       int32_t neg;
-      if (A.mode == WV_PAIRS_NATIVE) {
+      if (D.mode == WV_PAIRS_NATIVE) {
         // Philox4x32 counter (position, epoch, j/2): two draws per call
         uint32_t rnd[4] = {(uint32_t)pos, (uint32_t)((uint64_t)pos >> 32), (uint32_t)epoch, (uint32_t)(j >> 1)};
-        philox4x32_10(rnd, (uint32_t)A.seed ^ 0xA5A5F00Du, (uint32_t)(A.seed >> 32) ^ 0x3C6EF372u);
+        philox4x32_10(rnd, (uint32_t)D.seed ^ 0xA5A5F00Du, (uint32_t)(D.seed >> 32) ^ 0x3C6EF372u);
         const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
-        const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)A.n_candidates);
-        neg = A.candidates ? A.candidates[ci] : (int32_t)ci;
+        const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)D.n_candidates);
+        neg = D.candidates ? D.candidates[ci] : (int32_t)ci;
       } else {
-        neg = A.negatives[pos * k + j];
+        neg = D.negatives[pos * k + j];
       }
       row[jj] = neg;
       group_claim(A, (uint32_t)(neg + A.V));
@@ -699,7 +717,12 @@ __global__ void __launch_bounds__(kPairThreads) sgns_gather_kernel(PairArgs A, c
 // entities) go to the CTA-per-row kernel; the rest to the warp-per-row one.
 constexpr int kLightMax = 16;
 constexpr int kHeavyThreads = 256;
-constexpr int kRankSortMax = 1024;  // heavy rows up to this many slots sort in shared memory
+constexpr int kHeavyGroup = 8;            // rows loaded together per warp in the heavy kernel
+constexpr int64_t kBitmapMaxWords = 12288;  // slot bitmap in shared memory: batches up to 393,216 items
+__host__ __device__ __forceinline__ uint32_t heavy_bitmap_words(int64_t items) {
+  const int64_t w = (items + 31) / 32;
+  return w <= kBitmapMaxWords ? (uint32_t)w : 0u;
+}
 
 // One record per unique (matrix, row) of the batch, built by group_segments.
 struct Segment {
@@ -807,6 +830,8 @@ struct OwnerArgs {
   uint8_t* modified_in;
   uint8_t* modified_out;
   double lr;
+  void* gsum;          // [items, d] per-segment gradient rows (split mode): light i at i, heavy h at items-1-h
+  int split;           // 1: the owner kernels write gsum and sgns_adam_kernel applies RowAdam
   int sparse;          // 1: RowAdam sparse mode; 0: write dense gradient rows
   void* dense_g_in;    // dense mode gradient staging [V,d]
   void* dense_g_out;
@@ -836,16 +861,14 @@ __device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, double bc1, double
   return (np_ != old) || (np_ != np_) ? T(1) : T(0);
 }
 
-// Sorted contribution value v -> (source row, coefficient): input-matrix rows
+// Contribution slot v -> (source row index, coefficient): input-matrix rows
 // take the pair's centre gradient row G[b] (coefficient 1); output-matrix rows
 // take coef * U[b] (the context's gpos or negative j's gneg).
 template <typename T>
-__device__ __forceinline__ void contribution(uint32_t v, bool side_out, int64_t B, int k, int d, const T* U,
-                                             const T* G, const T* coef, const T*& src, T& c) {
+__device__ __forceinline__ uint32_t contribution(uint32_t v, bool side_out, int64_t B, int k, const T* coef, T& c) {
   if (!side_out) {
-    src = G + (int64_t)v * d;
     c = 1;
-    return;
+    return v;  // G row
   }
   const uint32_t s = v - (uint32_t)B;
   uint32_t pp, j;
@@ -857,8 +880,8 @@ __device__ __forceinline__ void contribution(uint32_t v, bool side_out, int64_t 
     pp = t / (uint32_t)k;
     j = 1 + t - pp * (uint32_t)k;
   }
-  src = U + (int64_t)pp * d;
   c = __ldg(coef + (int64_t)pp * (k + 1) + j);
+  return pp;  // U row
 }
 
 // Phase 3: one warp per (unique row, 32-chunk slice of the row): sum the row's
@@ -867,7 +890,7 @@ __device__ __forceinline__ void contribution(uint32_t v, bool side_out, int64_t 
 // so many warps are resident; the optimizer-state loads are issued before the
 // contribution walk so their DRAM latency overlaps it.
 template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(kOwnerThreads, 4) sgns_owner_kernel(OwnerArgs A) {
+__global__ void __launch_bounds__(kOwnerThreads, WV_OWNER_MINB) sgns_owner_kernel(OwnerArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t warps_total = (int64_t)gridDim.x * (kOwnerThreads / 32);
   const int64_t gw = blockIdx.x * (int64_t)(kOwnerThreads / 32) + (threadIdx.x >> 5);
@@ -889,60 +912,94 @@ __global__ void __launch_bounds__(kOwnerThreads, 4) sgns_owner_kernel(OwnerArgs 
   const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
   const T lr = (T)A.lr;
   const int64_t slots = (int64_t)nseg * MAXC;
+  // Per-row metadata (segment record -> slot list -> coefficients) is a chain
+  // of dependent L2 reads; the next row's chain is resolved while this row's
+  // optimizer-state loads are in flight (software pipelining across rows).
+  struct Meta {
+    uint32_t start, len, key;
+    double bc1, bc2;
+    uint32_t myslot, my_ri;
+    T my_c;
+  };
+  auto load_meta = [&](int64_t sl, Meta& mt) {
+    const Segment sg = A.segs[sl / MAXC];
+    mt.start = sg.start;
+    mt.len = sg.len;
+    mt.key = sg.key;
+    mt.bc1 = sg.bc1;
+    mt.bc2 = sg.bc2;
+    mt.myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
+    mt.my_c = 0;
+    mt.my_ri = 0;
+    if (lane < (int)sg.len) mt.my_ri = contribution<T>(mt.myslot, sg.key >= (uint32_t)A.V, B, k, coef, mt.my_c);
+  };
+  Meta nxt;
+  if (gw < slots) load_meta(gw, nxt);
   for (int64_t slot = gw; slot < slots; slot += warps_total) {
-    const int64_t sgi = slot / MAXC;
-    const int cc = (int)(slot - sgi * MAXC) * 32 + lane;
-    const Segment sg = A.segs[sgi];
-    const uint32_t key = sg.key;
+    const Meta cur = nxt;
+    const int cc = (int)(slot % MAXC) * 32 + lane;
+    Segment sg;
+    sg.start = cur.start;
+    sg.len = cur.len;
+    sg.bc1 = cur.bc1;
+    sg.bc2 = cur.bc2;
+    const uint32_t key = cur.key;
     const bool side_out = key >= (uint32_t)A.V;
     const int64_t row = side_out ? (int64_t)key - A.V : (int64_t)key;
     const bool active = cc < C;
-    // the row's (<= kLightMax) slots, ranked so they are summed in slot order
-    const uint32_t myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
-    int myrank = 0;
-    for (int j = 0; j < (int)sg.len; ++j) myrank += __shfl_sync(0xffffffffu, myslot, j) < myslot;
+    const uint32_t myslot = cur.myslot;
+    const T my_c = cur.my_c;
+    const uint32_t my_ri = cur.my_ri;
     T* P = (T*)(side_out ? A.out : A.in);
     T* M = (T*)(side_out ? A.m_out : A.m_in);
     T* Vv = (T*)(side_out ? A.v_out : A.v_in);
     const int64_t o = row * d + (int64_t)cc * EPC;
     Chunk<T, EPC> p, m, vv, g;
-    if (A.sparse && active) {
+    if (A.sparse && !A.split && active) {
       p = ld_chunk_rw<T, EPC>(P + o);
       m = ld_chunk_rw<T, EPC>(M + o);
       vv = ld_chunk_rw<T, EPC>(Vv + o);
     }
+    // next row's metadata while this row's state loads are in flight
+    if (slot + warps_total < slots) load_meta(slot + warps_total, nxt);
+    int myrank = 0;
+    for (int j = 0; j < (int)sg.len; ++j) myrank += __shfl_sync(0xffffffffu, myslot, j) < myslot;
 #pragma unroll
     for (int e = 0; e < EPC; ++e) g.v[e] = 0;
-    // contributions in groups of 4: all loads of a group are issued before the
-    // (slot-ordered) adds, so a row's walk costs len/4 dependent round trips
-    for (uint32_t i0 = 0; i0 < sg.len; i0 += 4) {
-      const int nq = (int)min(4u, sg.len - i0);
-      const T* src[4];
-      T c[4];
+    // contributions in groups of kOwnerGroup: all loads of a group are issued before the
+    // (slot-ordered) adds, so a row's walk costs len/kOwnerGroup dependent round trips
+    for (uint32_t i0 = 0; i0 < sg.len; i0 += kOwnerGroup) {
+      const int nq = (int)min((uint32_t)kOwnerGroup, sg.len - i0);
+      uint32_t ri[kOwnerGroup];
+      T c[kOwnerGroup];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kOwnerGroup; ++q) {
         const uint32_t owner = __ballot_sync(0xffffffffu, myrank == (int)i0 + q && lane < (int)sg.len);
-        const uint32_t v = __shfl_sync(0xffffffffu, myslot, owner ? __ffs(owner) - 1 : 0);
-        src[q] = nullptr;
-        c[q] = 0;
-        if (q < nq) contribution<T>(v, side_out, B, k, d, U, G, coef, src[q], c[q]);
+        const int src_lane = owner ? __ffs(owner) - 1 : 0;
+        ri[q] = __shfl_sync(0xffffffffu, my_ri, src_lane);
+        c[q] = __shfl_sync(0xffffffffu, my_c, src_lane);
       }
-      Chunk<T, EPC> x[4];
+      const T* srcb = (side_out ? U : G) + cc * EPC;
+      Chunk<T, EPC> x[kOwnerGroup];
       if (active) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q < nq) x[q] = ld_chunk<T, EPC>(src[q] + cc * EPC);
+        for (int q = 0; q < kOwnerGroup; ++q)
+          if (q < nq) x[q] = ld_chunk<T, EPC>(srcb + (size_t)ri[q] * d);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kOwnerGroup; ++q)
           if (q < nq) {
 #pragma unroll
             for (int e = 0; e < EPC; ++e) g.v[e] = add_rn(g.v[e], side_out ? mul_rn(c[q], x[q].v[e]) : x[q].v[e]);
           }
       }
     }
-    if (!A.sparse) {
-      T* D = (T*)(side_out ? A.dense_g_out : A.dense_g_in);
-      if (active) st_chunk<T, EPC>(D + o, g);
+    if (!A.sparse || A.split) {
+      if (!A.sparse) {
+        T* D = (T*)(side_out ? A.dense_g_out : A.dense_g_in);
+        if (active) st_chunk<T, EPC>(D + o, g);
+      } else if (active) {
+        st_chunk<T, EPC>((T*)A.gsum + (slot / MAXC) * d + (int64_t)cc * EPC, g);
+      }
       if (lane == 0 && cc == 0) {
         (side_out ? A.touched_out : A.touched_in)[row] = 1;
         A.cnt[key] = 0;
@@ -965,6 +1022,193 @@ __global__ void __launch_bounds__(kOwnerThreads, 4) sgns_owner_kernel(OwnerArgs 
       }
       if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
     }
+  }
+}
+
+// Phase 3 (default for 16-byte-multiple rows): warp per light row with the
+// row's optimizer state (p, m, v) fetched by cp.async.bulk into a per-warp
+// two-stage shared-memory ring: while row i is summed and updated, row i+1's
+// state is already in flight and row i+2's metadata chain is resolving, so
+// each warp keeps a full row of DRAM reads outstanding without holding it in
+// registers.  Updated rows are written straight back from registers.
+constexpr int kOwnerBulkWarps = 8;
+constexpr int kOwnerBulkX = 2;                 // contribution rows fetched with the state rows
+constexpr int kOwnerBulkRows = 3 + kOwnerBulkX;  // p, m, v, x0, x1
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(kOwnerBulkWarps * 32) sgns_owner_bulk_kernel(OwnerArgs A) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = A.d, k = A.k;
+  const int C = d / EPC;
+  const int64_t B = A.B;
+  const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
+  uint64_t* mybar = reinterpret_cast<uint64_t*>(smem_raw) + 2 * warp;
+  T* ring = reinterpret_cast<T*>(smem_raw + 128) + (size_t)warp * 2 * kOwnerBulkRows * d;
+  const uint32_t nseg = *A.seg_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    WvSgnsDevState* st = A.state;
+    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)nseg);
+    st->lo += B;
+    st->batch += 1;
+    st->step += 1;
+  }
+  if (lane == 0) {
+    mbar_init(mybar, 1);
+    mbar_init(mybar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const T* U = (const T*)A.U;
+  const T* G = (const T*)A.G;
+  const T* coef = (const T*)A.coef;
+  const T lr = (T)A.lr;
+  const int64_t warps_total = (int64_t)gridDim.x * kOwnerBulkWarps;
+  // a row's metadata: lane j holds contribution j (slot-order rank, source row, coefficient)
+  struct Meta {
+    uint32_t len, key;
+    double bc1, bc2;
+    int myrank;
+    uint32_t my_ri;
+    T my_c;
+  };
+  auto load_meta = [&](int64_t sgi, Meta& mt) {
+    const Segment sg = A.segs[sgi];
+    mt.len = sg.len;
+    mt.key = sg.key;
+    mt.bc1 = sg.bc1;
+    mt.bc2 = sg.bc2;
+    const uint32_t myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
+    mt.my_c = 0;
+    mt.my_ri = 0;
+    if (lane < (int)sg.len) mt.my_ri = contribution<T>(myslot, sg.key >= (uint32_t)A.V, B, k, coef, mt.my_c);
+    int r = 0;
+    for (int j = 0; j < (int)sg.len; ++j) r += __shfl_sync(0xffffffffu, myslot, j) < myslot;
+    mt.myrank = lane < (int)sg.len ? r : 64;
+  };
+  // contribution of rank q: (source row, coefficient)
+  auto ranked = [&](const Meta& mt, int q, uint32_t& ri, T& c) {
+    const uint32_t owner = __ballot_sync(0xffffffffu, mt.myrank == q);
+    const int src_lane = owner ? __ffs(owner) - 1 : 0;
+    ri = __shfl_sync(0xffffffffu, mt.my_ri, src_lane);
+    c = __shfl_sync(0xffffffffu, mt.my_c, src_lane);
+  };
+  auto issue = [&](const Meta& mt, int stage) {
+    const bool so = mt.key >= (uint32_t)A.V;
+    const int64_t row = so ? (int64_t)mt.key - A.V : (int64_t)mt.key;
+    const int nx = (int)min((uint32_t)kOwnerBulkX, mt.len);
+    uint32_t rx[kOwnerBulkX];
+#pragma unroll
+    for (int q = 0; q < kOwnerBulkX; ++q) {
+      T cq;
+      ranked(mt, q, rx[q], cq);
+    }
+    if (lane == 0) mbar_arrive_expect_tx(mybar + stage, (uint32_t)(3 + nx) * row_bytes);
+    __syncwarp();
+    T* dst = ring + (size_t)stage * kOwnerBulkRows * d;
+    if (lane < 3) {
+      const T* base = (const T*)(lane == 0 ? (so ? A.out : A.in) : lane == 1 ? (so ? A.m_out : A.m_in)
+                                                                             : (so ? A.v_out : A.v_in));
+      bulk_row_g2s(dst + (size_t)lane * d, base + row * d, row_bytes, mybar + stage);
+    } else if (lane < 3 + nx) {
+      const int q = lane - 3;
+      uint32_t r = rx[0];
+#pragma unroll
+      for (int t = 1; t < kOwnerBulkX; ++t)
+        if (q == t) r = rx[t];
+      bulk_row_g2s(dst + (size_t)lane * d, (so ? U : G) + (size_t)r * d, row_bytes, mybar + stage);
+    }
+  };
+  int64_t sgi = blockIdx.x * (int64_t)kOwnerBulkWarps + warp;
+  Meta cur, nxt;
+  uint32_t phase[2] = {0u, 0u};
+  if (sgi < nseg) {
+    load_meta(sgi, cur);
+    issue(cur, 0);
+    if (sgi + warps_total < nseg) load_meta(sgi + warps_total, nxt);
+  }
+  for (int it = 0; sgi < nseg; ++it, sgi += warps_total) {
+    const int stage = it & 1;
+    const bool have_next = sgi + warps_total < nseg;
+    if (have_next) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nxt, stage ^ 1);
+    }
+    const Meta m0 = cur;
+    if (have_next) {
+      cur = nxt;
+      if (sgi + 2 * warps_total < nseg) load_meta(sgi + 2 * warps_total, nxt);
+    }
+    const bool side_out = m0.key >= (uint32_t)A.V;
+    const int64_t row = side_out ? (int64_t)m0.key - A.V : (int64_t)m0.key;
+    const int nx = (int)min((uint32_t)kOwnerBulkX, m0.len);
+    T cx[kOwnerBulkX];
+#pragma unroll
+    for (int q = 0; q < kOwnerBulkX; ++q) {
+      uint32_t rq;
+      ranked(m0, q, rq, cx[q]);
+    }
+    while (!mbar_try_wait(mybar + stage, phase[stage])) {
+    }
+    phase[stage] ^= 1u;
+    const T* sp = ring + (size_t)stage * kOwnerBulkRows * d;
+    Chunk<T, EPC> g[MAXC];
+#pragma unroll
+    for (int qq = 0; qq < MAXC; ++qq) {
+      const int cc = lane + 32 * qq;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) g[qq].v[e] = 0;
+      if (cc < C) {
+#pragma unroll
+        for (int q = 0; q < kOwnerBulkX; ++q)
+          if (q < nx) {
+            const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(sp + (size_t)(3 + q) * d + cc * EPC);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(cx[q], x.v[e]) : x.v[e]);
+          }
+      }
+    }
+    // contributions past the first kOwnerBulkX (rare for light rows): plain loads, slot order
+    const T* srcb = side_out ? U : G;
+    for (int q = kOwnerBulkX; q < (int)m0.len; ++q) {
+      uint32_t rq;
+      T cq;
+      ranked(m0, q, rq, cq);
+#pragma unroll
+      for (int qq = 0; qq < MAXC; ++qq) {
+        const int cc = lane + 32 * qq;
+        if (cc < C) {
+          const Chunk<T, EPC> x = ld_chunk<T, EPC>(srcb + (size_t)rq * d + cc * EPC);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(cq, x.v[e]) : x.v[e]);
+        }
+      }
+    }
+    T* P = (T*)(side_out ? A.out : A.in);
+    T* M = (T*)(side_out ? A.m_out : A.m_in);
+    T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    bool changed = false;
+#pragma unroll
+    for (int qq = 0; qq < MAXC; ++qq) {
+      const int cc = lane + 32 * qq;
+      if (cc < C) {
+        Chunk<T, EPC> p = *reinterpret_cast<const Chunk<T, EPC>*>(sp + cc * EPC);
+        Chunk<T, EPC> m = *reinterpret_cast<const Chunk<T, EPC>*>(sp + d + cc * EPC);
+        Chunk<T, EPC> vv = *reinterpret_cast<const Chunk<T, EPC>*>(sp + 2 * d + cc * EPC);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g[qq].v[e], m0.bc1, m0.bc2, lr) != T(0);
+        const int64_t o = row * d + (int64_t)cc * EPC;
+        st_chunk<T, EPC>(P + o, p);
+        st_chunk<T, EPC>(M + o, m);
+        st_chunk<T, EPC>(Vv + o, vv);
+      }
+    }
+    changed = __any_sync(0xffffffffu, changed);
+    if (lane == 0) {
+      (side_out ? A.touched_out : A.touched_in)[row] = 1;
+      A.cnt[m0.key] = 0;
+      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+    }
+    __syncwarp();
   }
 }
 
@@ -1038,10 +1282,11 @@ __device__ uint32_t* cta_sort_slots(uint32_t* a, uint32_t* tmp, uint32_t n, int 
 template <typename T, int EPC, int MAXC>
 __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) {
   constexpr int W = kHeavyThreads / 32;
-  extern __shared__ unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   T* part = reinterpret_cast<T*>(smem_raw);  // [W][d]
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem_raw + (size_t)W * A.d * sizeof(T));
+  const uint32_t bitmap_words = heavy_bitmap_words(A.n_items);
   __shared__ uint32_t sort_hist[kHeavyThreads / 32][256];
-  __shared__ uint32_t rank_in[kRankSortMax], rank_out[kRankSortMax];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = A.d, k = A.k;
   const int C = d / EPC;
@@ -1059,57 +1304,80 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
     const uint32_t key = sg.key;
     const bool side_out = key >= (uint32_t)A.V;
     const int64_t row = side_out ? (int64_t)key - A.V : (int64_t)key;
-    // restore slot order of the row's list (stable LSD radix sort, ping-pong
-    // with the scratch list at the same offsets)
+    // restore slot order of the row's list: a bitmap over the batch's slot
+    // space (set bits, prefix popcounts, emit in order) when it fits in shared
+    // memory, else a CTA radix sort; either way the result is in slot order
     const uint32_t* sorted;
-    if (sg.len <= (uint32_t)kRankSortMax) {
-      // rank sort in shared memory: out[#smaller] = x (slots are distinct)
-      for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads) rank_in[i] = A.list[sg.start + i];
+    if (bitmap_words > 0) {
+      for (uint32_t i = threadIdx.x; i < bitmap_words; i += kHeavyThreads) bitmap[i] = 0u;
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads) {
-        const uint32_t x = rank_in[i];
-        uint32_t r = 0;
-        for (uint32_t j = 0; j < sg.len; ++j) r += rank_in[j] < x;
-        rank_out[r] = x;
+        const uint32_t x = A.list[sg.start + i];
+        atomicOr(&bitmap[x >> 5], 1u << (x & 31));
       }
       __syncthreads();
-      sorted = rank_out;
+      const uint32_t per_t = (bitmap_words + kHeavyThreads - 1) / kHeavyThreads;
+      const uint32_t w0 = min(bitmap_words, threadIdx.x * per_t), w1 = min(bitmap_words, w0 + per_t);
+      uint32_t mine = 0;
+      for (uint32_t w = w0; w < w1; ++w) mine += __popc(bitmap[w]);
+      __shared__ uint32_t scan_total;
+      uint32_t pos = block_excl_scan<uint32_t, kHeavyThreads>(mine, &scan_total);
+      uint32_t* out_sorted = A.list_tmp + sg.start;
+      for (uint32_t w = w0; w < w1; ++w) {
+        uint32_t bits = bitmap[w];
+        while (bits) {
+          const int bt = __ffs(bits) - 1;
+          out_sorted[pos++] = w * 32u + (uint32_t)bt;
+          bits &= bits - 1u;
+        }
+      }
+      __syncthreads();
+      sorted = out_sorted;
     } else {
       sorted = cta_sort_slots(const_cast<uint32_t*>(A.list) + sg.start, A.list_tmp + sg.start, sg.len, A.slot_bits,
                               sort_hist);
     }
+    // warp w sums the w-th contiguous part of the sorted list: 32 slots and
+    // their coefficients are fetched per lane at once, then the rows are
+    // loaded kHeavyGroup at a time and added in slot order
     const uint32_t per = (sg.len + W - 1) / W;
     const uint32_t lo = min(sg.len, per * warp), hi = min(sg.len, per * (warp + 1));
+    const T* srcb = side_out ? U : G;
     Chunk<T, EPC> g[MAXC];
 #pragma unroll
     for (int q = 0; q < MAXC; ++q)
 #pragma unroll
       for (int e = 0; e < EPC; ++e) g[q].v[e] = 0;
-    for (uint32_t i0 = lo; i0 < hi; i0 += 4) {
-      const int nq = (int)min(4u, hi - i0);
-      const T* src[4];
-      T c[4];
+    for (uint32_t i0 = lo; i0 < hi; i0 += 32) {
+      const uint32_t n32 = min(32u, hi - i0);
+      T my_c = 0;
+      uint32_t my_ri = 0;
+      if ((uint32_t)lane < n32) my_ri = contribution<T>(sorted[i0 + lane], side_out, B, k, coef, my_c);
+      for (uint32_t j0 = 0; j0 < n32; j0 += kHeavyGroup) {
+        const int nq = (int)min((uint32_t)kHeavyGroup, n32 - j0);
+        uint32_t ri[kHeavyGroup];
+        T c[kHeavyGroup];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        src[q] = nullptr;
-        c[q] = 0;
-        if (q < nq) contribution<T>(sorted[i0 + q], side_out, B, k, d, U, G, coef, src[q], c[q]);
-      }
+        for (int q = 0; q < kHeavyGroup; ++q) {
+          ri[q] = __shfl_sync(0xffffffffu, my_ri, (j0 + q) & 31);
+          c[q] = __shfl_sync(0xffffffffu, my_c, (j0 + q) & 31);
+        }
 #pragma unroll
-      for (int qq = 0; qq < MAXC; ++qq) {
-        const int cc = lane + 32 * qq;
-        if (cc < C) {
-          Chunk<T, EPC> x[4];
+        for (int qq = 0; qq < MAXC; ++qq) {
+          const int cc = lane + 32 * qq;
+          if (cc < C) {
+            Chunk<T, EPC> x[kHeavyGroup];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < nq) x[q] = ld_chunk<T, EPC>(src[q] + cc * EPC);
+            for (int q = 0; q < kHeavyGroup; ++q)
+              if (q < nq) x[q] = ld_chunk<T, EPC>(srcb + (size_t)ri[q] * d + cc * EPC);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < nq) {
+            for (int q = 0; q < kHeavyGroup; ++q)
+              if (q < nq) {
 #pragma unroll
-              for (int e = 0; e < EPC; ++e)
-                g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(c[q], x[q].v[e]) : x[q].v[e]);
-            }
+                for (int e = 0; e < EPC; ++e)
+                  g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(c[q], x[q].v[e]) : x[q].v[e]);
+              }
+          }
         }
       }
     }
@@ -1135,6 +1403,10 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
         ((T*)(side_out ? A.dense_g_out : A.dense_g_in))[o] = gr;
         continue;
       }
+      if (A.split) {
+        ((T*)A.gsum)[(A.n_items - 1 - (int64_t)h) * d + e] = gr;
+        continue;
+      }
       T p = P[o], m = M[o], vv = Vv[o];
       changed |= adam_elem<T>(p, m, vv, gr, sg.bc1, sg.bc2, lr) != T(0);
       P[o] = p;
@@ -1144,10 +1416,47 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
     changed = __syncthreads_or(changed);
     if (threadIdx.x == 0) {
       (side_out ? A.touched_out : A.touched_in)[row] = 1;
-      if (changed && A.sparse) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+      if (changed && A.sparse && !A.split) (side_out ? A.modified_out : A.modified_in)[row] = 1;
       A.cnt[key] = 0;
     }
     __syncthreads();  // shared buffers are reused by the next heavy row
+  }
+}
+
+// Phase 3c (split mode): RowAdam over every touched row, thread per 16-byte
+// chunk.  The row gradients were summed by the owner kernels into gsum, so
+// this pass is a pure stream of independent p/m/v/g loads and p/m/v stores
+// (the access pattern that runs closest to HBM bandwidth).
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(256) sgns_adam_kernel(OwnerArgs A) {
+  const int d = A.d;
+  const int C = d / EPC;
+  const uint32_t nl = A.seg_count[0], nh = A.seg_count[1];
+  const int64_t total = (int64_t)(nl + nh) * C;
+  const T lr = (T)A.lr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sgi = i / C;
+    const int c = (int)(i - sgi * C);
+    const bool heavy_row = sgi >= nl;
+    const Segment sg = heavy_row ? A.heavy[sgi - nl] : A.segs[sgi];
+    const int64_t grow = heavy_row ? A.n_items - 1 - (sgi - nl) : sgi;
+    const bool side_out = sg.key >= (uint32_t)A.V;
+    const int64_t row = side_out ? (int64_t)sg.key - A.V : (int64_t)sg.key;
+    T* P = (T*)(side_out ? A.out : A.in);
+    T* M = (T*)(side_out ? A.m_out : A.m_in);
+    T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    const int64_t o = row * d + (int64_t)c * EPC;
+    Chunk<T, EPC> p = ld_chunk_rw<T, EPC>(P + o);
+    Chunk<T, EPC> m = ld_chunk_rw<T, EPC>(M + o);
+    Chunk<T, EPC> vv = ld_chunk_rw<T, EPC>(Vv + o);
+    const Chunk<T, EPC> g = ld_chunk_rw<T, EPC>((const T*)A.gsum + grow * d + (int64_t)c * EPC);
+    bool changed = false;
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], sg.bc1, sg.bc2, lr) != T(0);
+    st_chunk<T, EPC>(P + o, p);
+    st_chunk<T, EPC>(M + o, m);
+    st_chunk<T, EPC>(Vv + o, vv);
+    if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
   }
 }
 
@@ -1384,8 +1693,23 @@ struct LaunchPair {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmemMax));
         attr_set[dev] = true;
       }
+      // persistent grid: exactly the resident CTAs (no partial second wave)
+      static int resident[16] = {0};
+      static size_t resident_smem[16] = {0};
+      int sms = 148;
+      if (dev >= 0 && dev < 16) {
+        if (resident[dev] == 0 || resident_smem[dev] != smem) {
+          int nb = 0;
+          WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_gather_bulk_kernel<T, EPC, MAXC>,
+                                                                 kBulkThreads, smem));
+          resident[dev] = nb > 0 ? nb : 1;
+          resident_smem[dev] = smem;
+        }
+        WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      }
       const int64_t blocks = (a.B + kBulkWarps - 1) / kBulkWarps;
-      const unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+      const int64_t cap = (int64_t)sms * (dev >= 0 && dev < 16 ? resident[dev] : 4);
+      const unsigned g = (unsigned)(blocks < cap ? blocks : cap);
       sgns_gather_bulk_kernel<T, EPC, MAXC><<<g, kBulkThreads, smem, st>>>(a, (const T*)in, (const T*)out);
     } else {
       sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
@@ -1425,6 +1749,7 @@ static cudaError_t side_stream(SideStream** out) {
 // Workspace of one SGNS replica: the persistent per-row counters first, then
 // the per-batch buffers.  With base == nullptr only the size is computed.
 struct BatchWs {
+  CorpusDesc* desc;
   uint32_t* cnt;
   uint32_t* gctr;
   void* U;
@@ -1437,6 +1762,7 @@ struct BatchWs {
   Segment* segs;
   Segment* heavy;
   double* partials;
+  void* gsum;
 };
 
 static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, int64_t es, BatchWs& w) {
@@ -1447,6 +1773,7 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, in
     off += al256(bytes);
     return p;
   };
+  w.desc = (CorpusDesc*)take(sizeof(CorpusDesc));
   w.cnt = (uint32_t*)take(2 * V * 4);
   w.gctr = (uint32_t*)take(64);
   w.U = take(B * d * es);
@@ -1459,13 +1786,54 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, in
   w.segs = (Segment*)take(items * (int64_t)sizeof(Segment));
   w.heavy = (Segment*)take((items / (kLightMax + 1) + 1) * (int64_t)sizeof(Segment));
   w.partials = (double*)take(148 * 32 * 8);
+  w.gsum = take(items * d * es);
   return off + 1024;
 }
+
+static CorpusDesc make_desc(const WvSgnsBatch* b) {
+  CorpusDesc c;
+  c.mode = b->mode;
+  c.window = b->window;
+  c.n_classes = (int)b->n_classes;
+  c.pad = 0;
+  c.N = b->n_pairs;
+  c.seed = b->seed;
+  c.tokens = b->tokens;
+  c.offsets = b->offsets;
+  c.class_len = b->class_len;
+  c.class_pair_start = b->class_pair_start;
+  c.class_walk_start = b->class_walk_start;
+  c.walks_by_class = b->walks_by_class;
+  c.candidates = b->candidates;
+  c.n_candidates = b->n_candidates;
+  c.pairs = b->pairs;
+  c.perm = b->perm;
+  c.negatives = b->negative_table;
+  return c;
+}
+
+template <typename T, int EPC, int MAXC>
+struct LaunchAdam {
+  static int run(const OwnerArgs& a, unsigned grid, cudaStream_t st) {
+    sgns_adam_kernel<T, EPC, MAXC><<<grid, 256, 0, st>>>(a);
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+};
 
 template <typename T, int EPC, int MAXC>
 struct LaunchHeavy {
   static int run(const OwnerArgs& a, unsigned grid, cudaStream_t st) {
-    sgns_heavy_kernel<T, EPC, MAXC><<<grid, kHeavyThreads, (kHeavyThreads / 32) * a.d * sizeof(T), st>>>(a);
+    const size_t smem = (kHeavyThreads / 32) * a.d * sizeof(T) + (size_t)heavy_bitmap_words(a.n_items) * 4;
+    static bool attr_set[16] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 16 && !attr_set[dev]) {
+      WV_CUDA(cudaFuncSetAttribute(sgns_heavy_kernel<T, EPC, MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((kHeavyThreads / 32) * 256 * 8 + kBitmapMaxWords * 4)));
+      attr_set[dev] = true;
+    }
+    sgns_heavy_kernel<T, EPC, MAXC><<<grid, kHeavyThreads, smem, st>>>(a);
     WV_LAUNCH_CHECK();
     return 0;
   }
@@ -1474,6 +1842,31 @@ struct LaunchHeavy {
 template <typename T, int EPC, int MAXC>
 struct LaunchOwner {
   static int run(const OwnerArgs& a, unsigned grid, cudaStream_t st) {
+    const size_t smem = 128 + (size_t)kOwnerBulkWarps * 2 * kOwnerBulkRows * a.d * sizeof(T);
+    if (a.sparse && !a.split && (a.d * sizeof(T)) % 16 == 0 && EPC * sizeof(T) == 16 && smem <= 112 * 1024 &&
+        getenv("WV_SGNS_REG_OWNER") == nullptr) {
+      static bool attr_set[16] = {false};
+      static int resident[16] = {0};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      int sms = 148;
+      if (dev >= 0 && dev < 16) {
+        if (!attr_set[dev]) {
+          WV_CUDA(cudaFuncSetAttribute(sgns_owner_bulk_kernel<T, EPC, MAXC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+          int nb = 0;
+          WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_owner_bulk_kernel<T, EPC, MAXC>,
+                                                                 kOwnerBulkWarps * 32, smem));
+          resident[dev] = nb > 0 ? nb : 1;
+          attr_set[dev] = true;
+        }
+        WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      const unsigned g = (unsigned)(sms * (dev >= 0 && dev < 16 ? resident[dev] : 2));
+      sgns_owner_bulk_kernel<T, EPC, MAXC><<<g, kOwnerBulkWarps * 32, smem, st>>>(a);
+      WV_LAUNCH_CHECK();
+      return 0;
+    }
     sgns_owner_kernel<T, EPC, MAXC><<<grid, kOwnerThreads, 0, st>>>(a);
     WV_LAUNCH_CHECK();
     return 0;
@@ -1673,6 +2066,23 @@ int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int v
   return 0;
 }
 
+// Write the corpus side of `batch` into the workspace (stream-ordered).  A
+// CUDA graph of batches captured against this workspace then trains on the
+// newly bound corpus when replayed.  wv_sgns_batch binds by itself when its
+// stream is not being captured.
+int wv_sgns_bind(const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size,
+                 int precision, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
+  BatchWs bw;
+  const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, batch->negatives, batch->batch_rows,
+                                      precision == WV_FP64 ? 8 : 4, bw);
+  WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
+  const CorpusDesc c = make_desc(batch);
+  WV_CUDA(cudaMemcpyAsync(bw.desc, &c, sizeof(c), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return 0;
+}
+
 // One SGNS batch: decode -> (gather || grouping) -> owner Adam phase.
 // Every launch is stream-ordered and reads the batch cursor from `state`, so
 // the sequence is CUDA-graph capturable and replayable.
@@ -1711,27 +2121,20 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   uint32_t* gctr = bw.gctr;
   uint32_t* seg_count = gctr + GC_LIGHT;
 
+  {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    WV_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusNone) {
+      const CorpusDesc c = make_desc(batch);
+      WV_CUDA(cudaMemcpyAsync(bw.desc, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+    }
+  }
   PairArgs pa;
-  pa.mode = batch->mode;
   pa.V = V;
   pa.d = d;
   pa.k = k;
-  pa.window = batch->window;
   pa.B = B;
-  pa.N = batch->n_pairs;
-  pa.seed = batch->seed;
-  pa.tokens = batch->tokens;
-  pa.offsets = batch->offsets;
-  pa.class_len = batch->class_len;
-  pa.class_pair_start = batch->class_pair_start;
-  pa.class_walk_start = batch->class_walk_start;
-  pa.n_classes = (int)batch->n_classes;
-  pa.walks_by_class = batch->walks_by_class;
-  pa.candidates = batch->candidates;
-  pa.n_candidates = batch->n_candidates;
-  pa.pairs = batch->pairs;
-  pa.perm = batch->perm;
-  pa.negatives = batch->negative_table;
+  pa.desc = bw.desc;
   pa.U = U;
   pa.G = G;
   pa.coef = coef;
@@ -1819,18 +2222,24 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.sparse = model->sparse;
   oa.dense_g_in = model->dense_g_in;
   oa.dense_g_out = model->dense_g_out;
+  oa.gsum = bw.gsum;
+  oa.split = (model->sparse && getenv("WV_SGNS_SPLIT_ADAM") != nullptr) ? 1 : 0;
   oa.state = model->state;
   const unsigned ogrid = grid_for(items * ((d + 127) / 128), kOwnerThreads / 32, 148 * 32);
   // heavy rows (side stream) and light rows (main stream) are disjoint: run both at once
   if (side == nullptr) WV_CUDA(side_stream(&side));
   WV_CUDA(cudaEventRecord(side->fork, st));
   WV_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
-  rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 2), side->s);
+  rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 4), side->s);
   if (rc) return rc;
   rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, ogrid, st);
   if (rc) return rc;
   WV_CUDA(cudaEventRecord(side->join, side->s));
   WV_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+  if (oa.split) {
+    rc = dispatch_rows<LaunchAdam>(model->precision, d, oa, (unsigned)(148 * 16), st);
+    if (rc) return rc;
+  }
   WV_STAMP(4, st);
 #undef WV_STAMP
   if (!model->sparse) {

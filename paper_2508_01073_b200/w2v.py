@@ -44,6 +44,9 @@ REPRODUCIBLE_SYNC_BATCHES = 64
 # device timestamps per profiled batch (WvSgnsBatch.timer): start, decode end,
 # gather end, join, owner end, sort start, sort end
 STAMPS_PER_BATCH = 7
+# (start, end) stamp pairs of the profiled phases: decode, gather, grouping (side stream), owner, whole batch
+_PHASE_SLOTS = ((0, 1), (1, 2), (5, 6), (3, 4), (0, 4))
+PHASE_NAMES = ("decode", "gather", "group", "owner", "batch")
 
 
 class TrainingDiverged(RuntimeError):
@@ -358,21 +361,43 @@ def generate_pairs(corpus, window_size: int, min_count: int, vocab_size: int | N
 
 # ---------------------------------------------------------------- trainer --
 class _Replica:
-    """One worker: its parameter store, its batch workspace and launch closures."""
+    """One worker: its parameter store, its batch workspace and launch closures.
+
+    The captured CUDA graphs depend only on the parameter store, the workspace
+    and the batch size: the corpus is read through the workspace's bound
+    descriptor, so ``retarget`` onto a new corpus keeps them (no recapture).
+    """
 
     def __init__(self, trainer, widx: int, params: _Params):
         self.t = trainer
         self.widx = widx
         self.p = params
         torch = trainer.torch
+        self.k = trainer.k
+        self.batch_size = trainer.batch_size
         self.ws = torch.empty(_lib.query("wv_sgns_batch_workspace_bytes", params.V, params.d, trainer.k,
                                          trainer.batch_size, params.precision), dtype=torch.uint8,
                               device=trainer.dev)
         _lib.call("wv_sgns_workspace_init", _lib.ptr(self.ws), self.ws.numel(), params.V, params.d, trainer.k,
                   trainer.batch_size, params.precision, _lib.stream_ptr())
         self.graphs = {}
-        self.graph_events = {}  # key -> DeviceTimer, STAMPS_PER_BATCH per batch, last replay (profiling)
         self.graph_launches = {}  # key -> kernels per replay
+        self.profile_samples = []  # [(decode, gather, group, owner, batch) ms] of profiled batches
+        self.bind()
+
+    def compatible(self, trainer) -> bool:
+        return trainer.k == self.k and trainer.batch_size <= self.batch_size
+
+    def retarget(self, trainer):
+        """Train the same replica on another corpus (same batch geometry)."""
+        self.t = trainer
+        self.bind()
+
+    def bind(self):
+        bs = self.t.batch_struct
+        bs.batch_rows = self.batch_size
+        _lib.call("wv_sgns_bind", C.byref(bs), _lib.ptr(self.ws), self.ws.numel(), self.p.V, self.p.d,
+                  self.p.precision, _lib.stream_ptr())
 
     def launch(self, rows: int, events=None):
         """One batch; ``events`` = (DeviceTimer, first slot): STAMPS_PER_BATCH device timestamps."""
@@ -391,11 +416,27 @@ class _Replica:
         finally:
             bs.timer, bs.timer_base = None, 0
 
+    def _profiled(self, count: int, rows: int, every: int = 16):
+        """Eager batches; one in ``every`` bracketed by device timestamps (no graph nodes distort it)."""
+        sampled = list(range(0, count, every))
+        timer = _lib.DeviceTimer(STAMPS_PER_BATCH * max(len(sampled), 1))
+        slot = {b: i for i, b in enumerate(sampled)}
+        for b in range(count):
+            i = slot.get(b)
+            self.launch(rows, None if i is None else (timer, STAMPS_PER_BATCH * i))
+        self.t.torch.cuda.current_stream().synchronize()
+        for i in range(len(sampled)):
+            o = STAMPS_PER_BATCH * i
+            self.profile_samples.append(tuple(timer.elapsed(o + a, o + b) for a, b in _PHASE_SLOTS))
+
     def run(self, count: int, rows: int):
         """``count`` consecutive batches of ``rows`` pairs, CUDA-graph replayed."""
         torch = self.t.torch
         G = self.t.graph_batches
         if count <= 0:
+            return
+        if self.t.profile:
+            self._profiled(count, rows)
             return
         if G <= 1 or count < 2:
             for _ in range(count):
@@ -405,15 +446,20 @@ class _Replica:
         reps, rem = divmod(count, key[1])
         if key not in self.graphs:
             g = torch.cuda.CUDAGraph()
-            evs = None
-            if self.t.profile:
-                evs = _lib.DeviceTimer(STAMPS_PER_BATCH * key[1])
             before = _lib.launch_count()
-            with torch.cuda.graph(g):
-                for i in range(key[1]):
-                    self.launch(rows, None if evs is None else (evs, STAMPS_PER_BATCH * i))
+            # capture on a side stream without torch.cuda.graph's gc.collect()/empty_cache()
+            cur = torch.cuda.current_stream()
+            cap = torch.cuda.Stream(device=self.t.dev)
+            cap.wait_stream(cur)
+            with torch.cuda.stream(cap):
+                g.capture_begin()
+                try:
+                    for _ in range(key[1]):
+                        self.launch(rows)
+                finally:
+                    g.capture_end()
+            cur.wait_stream(cap)
             self.graphs[key] = g
-            self.graph_events[key] = evs
             self.graph_launches[key] = _lib.launch_count() - before
             _lib.note_graph_replay(-self.graph_launches[key])  # the capture itself runs nothing
         g = self.graphs[key]
@@ -708,7 +754,11 @@ class SkipGramSession:
         tr = _Trainer(corpus, self.V, cfg, self.seed, self.events, self.precision, "device", self.graph_batches,
                       device=self.dev)
         tr.profile = profile
-        rep = _Replica(tr, 0, self.params)
+        rep = self.last_replica
+        if rep is not None and rep.compatible(tr):
+            rep.retarget(tr)
+        else:
+            rep = _Replica(tr, 0, self.params)
         self.last_replica = rep
         B, N = tr.batch_size, tr.N
         full, rem = divmod(N, B)
