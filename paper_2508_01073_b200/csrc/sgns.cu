@@ -813,6 +813,7 @@ struct OwnerArgs {
   uint32_t* list_tmp;    // scratch for the heavy rows' slot sort
   uint32_t* cnt;         // reset to 0 per row once consumed
   int slot_bits;         // bits of the largest slot (2B + Bk - 1)
+  uint32_t kmag;         // ~2^32 / k for the slot -> (pair, negative) split
   const Segment* segs;
   const Segment* heavy;
   const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
@@ -843,19 +844,49 @@ struct OwnerArgs {
 // divisions); the float32 store multiplies by the per-row reciprocals of the
 // bias corrections and uses a fast divide (a few ulp; the fp32 store is
 // tolerance-checked against the reference, not bit-checked).
+// Per-row bias corrections in the form the element update consumes: float64
+// keeps 1 - b^t (divided by, numpy order); float32 keeps their reciprocals.
 template <typename T>
-__device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, double bc1, double bc2, T lr) {
+struct AdamBC {
+  double bc1, bc2;
+  __device__ __forceinline__ AdamBC(double a, double b) : bc1(a), bc2(b) {}
+};
+template <>
+struct AdamBC<float> {
+  float r1, r2;
+  __device__ __forceinline__ AdamBC(double a, double b) {
+#ifdef __CUDA_ARCH__
+    r1 = __frcp_rn((float)a);
+    r2 = __frcp_rn((float)b);
+#endif
+  }
+};
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// RowAdam element update (w2v.py:384-395): m, v recurrences, bias-corrected
+// step.  float64 keeps numpy's exact operation order (correctly rounded
+// divisions, no FMA contraction).  The float32 store uses FMAs, the per-row
+// reciprocals of the bias corrections and approximate sqrt / divide (a few
+// ulp; the fp32 store is tolerance-checked against the reference).
+template <typename T>
+__device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, const AdamBC<T>& bc, T lr) {
   const T b1 = (T)0.9, b2 = (T)0.999, omb1 = (T)(1.0 - 0.9), omb2 = (T)(1.0 - 0.999), eps = (T)1e-8;
-  m = add_rn(mul_rn(b1, m), mul_rn(omb1, g));
-  v = add_rn(mul_rn(b2, v), mul_rn(mul_rn(omb2, g), g));
   T upd;
   if constexpr (sizeof(T) == 8) {
-    upd = div_rn(mul_rn(lr, div_rn(m, (T)bc1)), add_rn(sqrt_rn(div_rn(v, (T)bc2)), eps));
+    m = add_rn(mul_rn(b1, m), mul_rn(omb1, g));
+    v = add_rn(mul_rn(b2, v), mul_rn(mul_rn(omb2, g), g));
+    upd = div_rn(mul_rn(lr, div_rn(m, (T)bc.bc1)), add_rn(sqrt_rn(div_rn(v, (T)bc.bc2)), eps));
   } else {
-    const float mh = m * (float)(1.0 / bc1), vh = v * (float)(1.0 / bc2);
-    upd = __fdividef(lr * mh, __fsqrt_rn(vh) + eps);
+    m = fmaf(b1, m, omb1 * g);
+    v = fmaf(b2, v, (omb2 * g) * g);
+    upd = __fdividef(lr * (m * bc.r1), sqrt_approx(v * bc.r2) + eps);
   }
-  const T np_ = sub_rn(p, upd);
+  const T np_ = p - upd;
   const T old = p;
   p = np_;
   return (np_ != old) || (np_ != np_) ? T(1) : T(0);
@@ -865,7 +896,8 @@ __device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, double bc1, double
 // take the pair's centre gradient row G[b] (coefficient 1); output-matrix rows
 // take coef * U[b] (the context's gpos or negative j's gneg).
 template <typename T>
-__device__ __forceinline__ uint32_t contribution(uint32_t v, bool side_out, int64_t B, int k, const T* coef, T& c) {
+__device__ __forceinline__ uint32_t contribution(uint32_t v, bool side_out, int64_t B, int k, uint32_t kmag,
+                                                 const T* coef, T& c) {
   if (!side_out) {
     c = 1;
     return v;  // G row
@@ -876,9 +908,18 @@ __device__ __forceinline__ uint32_t contribution(uint32_t v, bool side_out, int6
     pp = s;
     j = 0;
   } else {
+    // t / k by multiply-high with a one-step correction (kmag ~ 2^32 / k)
     const uint32_t t = s - (uint32_t)B;
-    pp = t / (uint32_t)k;
-    j = 1 + t - pp * (uint32_t)k;
+    pp = __umulhi(t, kmag);
+    int32_t r = (int32_t)(t - pp * (uint32_t)k);
+    if (r < 0) {
+      --pp;
+      r += k;
+    } else if (r >= k) {
+      ++pp;
+      r -= k;
+    }
+    j = 1 + (uint32_t)r;
   }
   c = __ldg(coef + (int64_t)pp * (k + 1) + j);
   return pp;  // U row
@@ -931,7 +972,7 @@ __global__ void __launch_bounds__(kOwnerThreads, WV_OWNER_MINB) sgns_owner_kerne
     mt.myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
     mt.my_c = 0;
     mt.my_ri = 0;
-    if (lane < (int)sg.len) mt.my_ri = contribution<T>(mt.myslot, sg.key >= (uint32_t)A.V, B, k, coef, mt.my_c);
+    if (lane < (int)sg.len) mt.my_ri = contribution<T>(mt.myslot, sg.key >= (uint32_t)A.V, B, k, A.kmag, coef, mt.my_c);
   };
   Meta nxt;
   if (gw < slots) load_meta(gw, nxt);
@@ -1006,10 +1047,11 @@ __global__ void __launch_bounds__(kOwnerThreads, WV_OWNER_MINB) sgns_owner_kerne
       }
       continue;
     }
+    const AdamBC<T> bc(sg.bc1, sg.bc2);
     bool changed = false;
     if (active) {
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], sg.bc1, sg.bc2, lr) != T(0);
+      for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], bc, lr) != T(0);
       st_chunk<T, EPC>(P + o, p);
       st_chunk<T, EPC>(M + o, m);
       st_chunk<T, EPC>(Vv + o, vv);
@@ -1032,10 +1074,10 @@ __global__ void __launch_bounds__(kOwnerThreads, WV_OWNER_MINB) sgns_owner_kerne
 // each warp keeps a full row of DRAM reads outstanding without holding it in
 // registers.  Updated rows are written straight back from registers.
 constexpr int kOwnerBulkWarps = 8;
-constexpr int kOwnerBulkX = 2;                 // contribution rows fetched with the state rows
+constexpr int kOwnerBulkX = 1;                 // contribution rows fetched with the state rows
 constexpr int kOwnerBulkRows = 3 + kOwnerBulkX;  // p, m, v, x0, x1
 template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(kOwnerBulkWarps * 32) sgns_owner_bulk_kernel(OwnerArgs A) {
+__global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kernel(OwnerArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = A.d, k = A.k;
@@ -1080,7 +1122,7 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32) sgns_owner_bulk_kernel(O
     const uint32_t myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
     mt.my_c = 0;
     mt.my_ri = 0;
-    if (lane < (int)sg.len) mt.my_ri = contribution<T>(myslot, sg.key >= (uint32_t)A.V, B, k, coef, mt.my_c);
+    if (lane < (int)sg.len) mt.my_ri = contribution<T>(myslot, sg.key >= (uint32_t)A.V, B, k, A.kmag, coef, mt.my_c);
     int r = 0;
     for (int j = 0; j < (int)sg.len; ++j) r += __shfl_sync(0xffffffffu, myslot, j) < myslot;
     mt.myrank = lane < (int)sg.len ? r : 64;
@@ -1186,6 +1228,7 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32) sgns_owner_bulk_kernel(O
     T* P = (T*)(side_out ? A.out : A.in);
     T* M = (T*)(side_out ? A.m_out : A.m_in);
     T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    const AdamBC<T> bc(m0.bc1, m0.bc2);
     bool changed = false;
 #pragma unroll
     for (int qq = 0; qq < MAXC; ++qq) {
@@ -1195,7 +1238,7 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32) sgns_owner_bulk_kernel(O
         Chunk<T, EPC> m = *reinterpret_cast<const Chunk<T, EPC>*>(sp + d + cc * EPC);
         Chunk<T, EPC> vv = *reinterpret_cast<const Chunk<T, EPC>*>(sp + 2 * d + cc * EPC);
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g[qq].v[e], m0.bc1, m0.bc2, lr) != T(0);
+        for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g[qq].v[e], bc, lr) != T(0);
         const int64_t o = row * d + (int64_t)cc * EPC;
         st_chunk<T, EPC>(P + o, p);
         st_chunk<T, EPC>(M + o, m);
@@ -1352,7 +1395,7 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
       const uint32_t n32 = min(32u, hi - i0);
       T my_c = 0;
       uint32_t my_ri = 0;
-      if ((uint32_t)lane < n32) my_ri = contribution<T>(sorted[i0 + lane], side_out, B, k, coef, my_c);
+      if ((uint32_t)lane < n32) my_ri = contribution<T>(sorted[i0 + lane], side_out, B, k, A.kmag, coef, my_c);
       for (uint32_t j0 = 0; j0 < n32; j0 += kHeavyGroup) {
         const int nq = (int)min((uint32_t)kHeavyGroup, n32 - j0);
         uint32_t ri[kHeavyGroup];
@@ -1393,6 +1436,7 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
     T* P = (T*)(side_out ? A.out : A.in);
     T* M = (T*)(side_out ? A.m_out : A.m_in);
     T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    const AdamBC<T> bc(sg.bc1, sg.bc2);
     bool changed = false;
     for (int e = threadIdx.x; e < d; e += kHeavyThreads) {
       T gr = part[e];
@@ -1408,7 +1452,7 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
         continue;
       }
       T p = P[o], m = M[o], vv = Vv[o];
-      changed |= adam_elem<T>(p, m, vv, gr, sg.bc1, sg.bc2, lr) != T(0);
+      changed |= adam_elem<T>(p, m, vv, gr, bc, lr) != T(0);
       P[o] = p;
       M[o] = m;
       Vv[o] = vv;
@@ -1450,9 +1494,10 @@ __global__ void __launch_bounds__(256) sgns_adam_kernel(OwnerArgs A) {
     Chunk<T, EPC> m = ld_chunk_rw<T, EPC>(M + o);
     Chunk<T, EPC> vv = ld_chunk_rw<T, EPC>(Vv + o);
     const Chunk<T, EPC> g = ld_chunk_rw<T, EPC>((const T*)A.gsum + grow * d + (int64_t)c * EPC);
+    const AdamBC<T> bc(sg.bc1, sg.bc2);
     bool changed = false;
 #pragma unroll
-    for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], sg.bc1, sg.bc2, lr) != T(0);
+    for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], bc, lr) != T(0);
     st_chunk<T, EPC>(P + o, p);
     st_chunk<T, EPC>(M + o, m);
     st_chunk<T, EPC>(Vv + o, vv);
@@ -2202,6 +2247,7 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.list_tmp = bw.list_tmp;
   oa.cnt = bw.cnt;
   oa.slot_bits = bits_for((uint64_t)(items - 1));
+  oa.kmag = k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)k + 1ull) : 0xFFFFFFFFu;
   oa.segs = segs;
   oa.heavy = heavy;
   oa.seg_count = seg_count;

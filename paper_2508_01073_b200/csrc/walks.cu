@@ -64,78 +64,185 @@ struct WalkParams {
   int32_t* lengths;
 };
 
-template <int RNG>
-__global__ void __launch_bounds__(kWalkThreads) random_walk_kernel(WalkParams P) {
+// Per-device table of the affine PCG64 jumps of n = 1..kShard steps: walker
+// row i of a shard starts from jump(i + 1) of the shard's seeded state (one
+// coalesced 32-byte load instead of a 13-step square-and-multiply per lane).
+static PcgJump* g_jump_rows[16] = {nullptr};
+
+__global__ void fill_jump_rows(PcgJump* tab) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < kShard) tab[n] = pcg_jump_dev((uint64_t)n + 1);
+}
+
+static cudaError_t ensure_jump_rows(PcgJump** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  if (g_jump_rows[dev] == nullptr) {
+    PcgJump* t = nullptr;
+    e = cudaMalloc(&t, sizeof(PcgJump) * kShard);
+    if (e != cudaSuccess) return e;
+    fill_jump_rows<<<kShard / 256, 256>>>(t);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+    g_jump_rows[dev] = t;
+  }
+  *out = g_jump_rows[dev];
+  return cudaSuccess;
+}
+
+// Generator state of one walker in flight.
+struct Walker {
+  u128 x;      // PCG64 state before its next draw
+  u128 cstep;  // inc * S of the per-hop stride
+  uint64_t i;  // row within the shard (Philox counter)
+  int64_t cur;
+  int len;
+  bool last;   // in the final (short) shard
+  bool alive;
+};
+
+// Random walks, WPT walkers per thread.  Walker w of the root-major work list
+// is row i = w mod 8192 of shard s = w / 8192; its draw for hop h is element
+// h * n_s + i of the shard's stream (walks.py:117-141, 166-173).  Two lanes
+// per CTA seed the (at most two) shards the CTA's walkers fall in
+// (SeedSequence -> PCG64 / Philox key, shared memory); each walker then jumps
+// to its row with one table load.  The
+// hop loop interleaves the thread's walkers so their dependent CSR reads
+// (offsets -> packed edge) overlap.  Rows are staged in shared memory and
+// written with 16-byte stores.
+template <int RNG, int WPT>
+__global__ void __launch_bounds__(kWalkThreads) random_walk_kernel(WalkParams P, const PcgJump* __restrict__ jrows) {
   extern __shared__ int32_t stage[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = P.width;
-  const int64_t wl = blockIdx.x * (int64_t)kWalkThreads + threadIdx.x;
-  int32_t* my = stage + (warp * 32 + lane) * width;
-  for (int j = 0; j < width; ++j) my[j] = -1;
-  int len = 0;
-  if (wl < P.work_count) {
-    const int64_t w = P.work_begin + wl;
-    const int64_t s = w / kShard;
-    const uint64_t i = (uint64_t)(w - s * kShard);
-    const bool last = (s == P.last_shard);
-    const uint64_t n_s = last ? (uint64_t)P.n_last : (uint64_t)kShard;
-    int64_t cur = P.roots[w / P.walk_number];
-    my[0] = (int32_t)cur;
-    len = 1;
+  const int64_t blk0 = blockIdx.x * (int64_t)kWalkThreads * WPT;
+  // the CTA's walkers span at most two shards (kWalkThreads * WPT <= kShard):
+  // lanes 0/1 of warp 0 seed them once for the whole CTA
+  __shared__ uint64_t sh_seed[2][4];  // PCG64: state.lo, state.hi, inc.lo, inc.hi; Philox: key
+  const int64_t s0 = (P.work_begin + blk0) / kShard;
+  if (warp == 0 && lane < 2) {
     uint32_t pool[4];
-    ss_pool(P.prefix, P.n_prefix, (uint64_t)s, pool);
-    u128 x{0, 0}, cstep{0, 0};
-    u128 astep{1, 0};
-    uint64_t k0 = 0, k1 = 0;
+    ss_pool(P.prefix, P.n_prefix, (uint64_t)(s0 + lane), pool);
     if (RNG == WV_RNG_PCG64) {
-      Pcg64 g = pcg_seed(pool);
-      PcgJump j = pcg_jump_dev(i + 1);
-      x = add128(mul128(j.A, g.state), mul128(g.inc, j.S));
-      const PcgJump& st = last ? P.stride_last : P.stride_full;
-      astep = st.A;
-      cstep = mul128(g.inc, st.S);
+      const Pcg64 g = pcg_seed(pool);
+      sh_seed[lane][0] = g.state.lo;
+      sh_seed[lane][1] = g.state.hi;
+      sh_seed[lane][2] = g.inc.lo;
+      sh_seed[lane][3] = g.inc.hi;
     } else {
       uint64_t key[2];
       ss_generate_u64(pool, 2, key);
-      k0 = key[0];
-      k1 = key[1];
+      sh_seed[lane][0] = key[0];
+      sh_seed[lane][1] = key[1];
     }
-    const int64_t* __restrict__ off = P.row_offsets;
-    const uint64_t* __restrict__ edges = P.edges;
-    for (int h = 0; h < P.depth; ++h) {
-      const int64_t lo = __ldg(off + cur), hi = __ldg(off + cur + 1);
-      if (hi == lo) break;
-      uint64_t u;
-      if (RNG == WV_RNG_PCG64) {
-        u = pcg_output(x);
-        x = add128(mul128(astep, x), cstep);
-      } else {
-        u = philox_numpy_u64(k0, k1, (uint64_t)h * n_s + i);
+  }
+  Walker W[WPT];
+  uint64_t k0[WPT], k1[WPT];
+  const PcgJump* jr[WPT];
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    // walker q of this thread: sub-block q, so each warp's 32 walkers are consecutive
+    const int64_t wl = blk0 + (int64_t)q * kWalkThreads + threadIdx.x;
+    int32_t* my = stage + ((q * kWalkThreads) + warp * 32 + lane) * width;
+    for (int j = 0; j < width; ++j) my[j] = -1;
+    W[q].alive = wl < P.work_count;
+    W[q].len = 0;
+    W[q].cur = 0;
+    const int64_t w = P.work_begin + (W[q].alive ? wl : 0);
+    const int64_t s = w / kShard;
+    W[q].i = (uint64_t)(w - s * kShard);
+    W[q].last = (s == P.last_shard);
+    jr[q] = jrows + W[q].i;  // i + 1 steps
+    if (W[q].alive) {
+      W[q].cur = P.roots[w / P.walk_number];
+      my[0] = (int32_t)W[q].cur;
+      W[q].len = 1;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t wl = blk0 + (int64_t)q * kWalkThreads + threadIdx.x;
+    const int src = W[q].alive ? (int)((P.work_begin + wl) / kShard - s0) : 0;
+    const uint64_t* sd = sh_seed[src];
+    if (RNG == WV_RNG_PCG64) {
+      const u128 state{sd[0], sd[1]}, inc{sd[2], sd[3]};
+      const PcgJump j = *jr[q];
+      W[q].x = add128(mul128(j.A, state), mul128(inc, j.S));
+      W[q].cstep = mul128(inc, W[q].last ? P.stride_last.S : P.stride_full.S);
+    } else {
+      k0[q] = sd[0];
+      k1[q] = sd[1];
+    }
+  }
+  const int64_t* __restrict__ off = P.row_offsets;
+  const uint64_t* __restrict__ edges = P.edges;
+  for (int h = 0; h < P.depth; ++h) {
+    int64_t lo[WPT], hi[WPT];
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      lo[q] = hi[q] = 0;
+      if (W[q].alive) {
+        lo[q] = __ldg(off + W[q].cur);
+        hi[q] = __ldg(off + W[q].cur + 1);
       }
-      const int64_t deg = hi - lo;
+    }
+    uint64_t e[WPT];
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      if (W[q].alive && hi[q] == lo[q]) W[q].alive = false;
+      uint64_t u = 0;
+      if (RNG == WV_RNG_PCG64) {
+        u = pcg_output(W[q].x);
+        W[q].x = add128(mul128(W[q].last ? P.stride_last.A : P.stride_full.A, W[q].x), W[q].cstep);
+      } else if (W[q].alive) {
+        const uint64_t n_s = W[q].last ? (uint64_t)P.n_last : (uint64_t)kShard;
+        u = philox_numpy_u64(k0[q], k1[q], (uint64_t)h * n_s + W[q].i);
+      }
+      const int64_t deg = hi[q] - lo[q];
       int64_t pick = __double2ll_rz(__dmul_rn(u64_to_double(u), (double)deg));
       if (pick > deg - 1) pick = deg - 1;
-      const uint64_t e = __ldg(edges + lo + pick);
-      my[2 * h + 1] = (int32_t)(e >> 32);
-      my[2 * h + 2] = (int32_t)(uint32_t)e;
-      cur = (int64_t)(uint32_t)e;
-      len += 2;
+      e[q] = W[q].alive ? __ldg(edges + lo[q] + pick) : 0ull;
     }
-    P.lengths[wl] = len;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      if (W[q].alive) {
+        int32_t* my = stage + ((q * kWalkThreads) + warp * 32 + lane) * width;
+        my[2 * h + 1] = (int32_t)(e[q] >> 32);
+        my[2 * h + 2] = (int32_t)(uint32_t)e[q];
+        W[q].cur = (int64_t)(uint32_t)e[q];
+        W[q].len += 2;
+      }
+    }
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) any |= W[q].alive;
+    if (!any) break;
+  }
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t wl = blk0 + (int64_t)q * kWalkThreads + threadIdx.x;
+    if (wl < P.work_count) P.lengths[wl] = W[q].len;
   }
   __syncwarp();
-  const int64_t wl0 = wl - lane;
-  if (wl0 >= P.work_count) return;
-  const int64_t nvalid = min((int64_t)32, P.work_count - wl0);
-  const int32_t* src = stage + warp * 32 * width;
-  int32_t* dst = P.corpus + wl0 * width;
-  const int total = (int)nvalid * width;
-  if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-    const int4* s4 = reinterpret_cast<const int4*>(src);
-    int4* d4 = reinterpret_cast<int4*>(dst);
-    for (int j = lane; j < total / 4; j += 32) d4[j] = s4[j];
-  } else {
-    for (int j = lane; j < total; j += 32) dst[j] = src[j];
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t wl0 = blk0 + (int64_t)q * kWalkThreads + warp * 32;
+    if (wl0 >= P.work_count) continue;
+    const int64_t nvalid = min((int64_t)32, P.work_count - wl0);
+    const int32_t* srcr = stage + ((q * kWalkThreads) + warp * 32) * width;
+    int32_t* dst = P.corpus + wl0 * width;
+    const int total = (int)nvalid * width;
+    if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      const int4* s4 = reinterpret_cast<const int4*>(srcr);
+      int4* d4 = reinterpret_cast<int4*>(dst);
+      for (int j = lane; j < total / 4; j += 32) d4[j] = s4[j];
+    } else {
+      for (int j = lane; j < total; j += 32) dst[j] = srcr[j];
+    }
   }
 }
 
@@ -301,20 +408,27 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, in
   P.stride_last = pcg_jump_n(tab, (uint64_t)P.n_last);
   P.corpus = corpus;
   P.lengths = lengths;
-  const size_t smem = (size_t)kWalkThreads * width * sizeof(int32_t);
-  const int64_t blocks = (work_count + kWalkThreads - 1) / kWalkThreads;
+  PcgJump* jrows = nullptr;
+  WV_CUDA(ensure_jump_rows(&jrows));
+  // two walkers per thread while their staged rows fit in shared memory
+  const bool two = (size_t)2 * kWalkThreads * width * sizeof(int32_t) <= 96 * 1024;
+  const int wpt = two ? 2 : 1;
+  const size_t smem = (size_t)wpt * kWalkThreads * width * sizeof(int32_t);
+  const int64_t per_block = (int64_t)kWalkThreads * wpt;
+  const int64_t blocks = (work_count + per_block - 1) / per_block;
   WV_CHECK_ARG(blocks < (1ll << 31), "too many walkers for one launch");
-  if (rng_kind == WV_RNG_PCG64) {
+  auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024)
-      WV_CUDA(cudaFuncSetAttribute(random_walk_kernel<WV_RNG_PCG64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    random_walk_kernel<WV_RNG_PCG64><<<(unsigned)blocks, kWalkThreads, smem, st>>>(P);
-  } else {
-    if (smem > 48 * 1024)
-      WV_CUDA(cudaFuncSetAttribute(random_walk_kernel<WV_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    random_walk_kernel<WV_RNG_PHILOX><<<(unsigned)blocks, kWalkThreads, smem, st>>>(P);
-  }
+      WV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)blocks, kWalkThreads, smem, st>>>(P, jrows);
+    return 0;
+  };
+  int rc;
+  if (rng_kind == WV_RNG_PCG64)
+    rc = two ? launch(random_walk_kernel<WV_RNG_PCG64, 2>) : launch(random_walk_kernel<WV_RNG_PCG64, 1>);
+  else
+    rc = two ? launch(random_walk_kernel<WV_RNG_PHILOX, 2>) : launch(random_walk_kernel<WV_RNG_PHILOX, 1>);
+  if (rc) return rc;
   WV_LAUNCH_CHECK();
   return 0;
 }
