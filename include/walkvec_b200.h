@@ -224,6 +224,12 @@ int wv_sgns_bind(const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t v
 int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size, int negatives,
                            int64_t batch, int precision, void* stream);
 int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream);
+/* `count` consecutive batches, software-pipelined over the workspace's two
+ * halves (decode + grouping of batch i+1 on a side stream while batch i is
+ * gathered and applied); equal to `count` wv_sgns_batch calls; capturable as
+ * one CUDA graph.  Replaces the batch loop of w2v._train_single (w2v.py:553-565). */
+int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t count,
+                    void* stream);
 #define WV_PHASE_PAIRS 1  /* decode pair/negative rows; gather rows, dots, coefficients, batch loss */
 #define WV_PHASE_GROUP 2  /* group contribution slots by destination row (no sort) */
 #define WV_PHASE_UPDATE 4 /* per unique row: slot-ordered sum + RowAdam */

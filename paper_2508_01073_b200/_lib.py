@@ -153,6 +153,7 @@ SIGNATURES = {
     "wv_sgns_bind": (I32, [P, P, I64, I64, I32, I32, P]),
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
+    "wv_sgns_batches": (I32, [P, P, P, I64, I64, P]),
     "wv_replica_delta": (I32, [P, P, I64, I32, P, P]),
     "wv_replica_apply": (I32, [P, P, P, P, I64, I32, I32, P]),
     "wv_barabasi_edge_count": (I64, [I64, I32]),

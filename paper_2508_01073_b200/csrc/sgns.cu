@@ -736,8 +736,11 @@ struct Segment {
 
 __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __restrict__ cnt, uint32_t* gctr,
                                int64_t V, int sparse, int32_t* __restrict__ steps_in, int32_t* __restrict__ steps_out,
-                               Segment* __restrict__ segs, Segment* __restrict__ heavy, int64_t max_unique) {
+                               Segment* __restrict__ segs, Segment* __restrict__ heavy, int64_t max_unique,
+                               WvSgnsDevState* state, int64_t B) {
   const int lane = threadIdx.x & 31;
+  // the batch's pairs are decoded: advance the decode cursor for the next batch
+  if (blockIdx.x == 0 && threadIdx.x == 0) state->lo += B;
   const uint32_t nu = *(volatile uint32_t*)(gctr + GC_UNIQUE);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nu && base < max_unique; base += stride) {
@@ -943,7 +946,6 @@ __global__ void __launch_bounds__(kOwnerThreads, WV_OWNER_MINB) sgns_owner_kerne
     // the batch is consumed: advance the cursor (read by the next batch's decode)
     WvSgnsDevState* st = A.state;
     atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)nseg);
-    st->lo += B;
     st->batch += 1;
     st->step += 1;
   }
@@ -1090,7 +1092,6 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     WvSgnsDevState* st = A.state;
     atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)nseg);
-    st->lo += B;
     st->batch += 1;
     st->step += 1;
   }
@@ -1764,13 +1765,16 @@ struct LaunchPair {
   }
 };
 
-// side stream + fork/join events (per host thread and device) so the grouping
-// sort runs concurrently with the gather kernel; works eagerly and under
-// CUDA-graph capture (the side stream joins the capture through the events)
+// Streams and events of the batch pipeline (per host thread and device):
+//   side  : decode + grouping of batch i+1 while the main stream runs batch i
+//   heavy : the CTA-per-heavy-row kernel, concurrent with the light-row owner
+// Works eagerly and under CUDA-graph capture: every side-stream segment forks
+// from and joins back into the caller's stream through these events.
 struct SideStream {
   int dev = -1;
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t s = nullptr, h = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, fork_h = nullptr, join_h = nullptr;
+  cudaEvent_t dec[2] = {nullptr, nullptr}, grp[2] = {nullptr, nullptr}, own[2] = {nullptr, nullptr};
 };
 
 static cudaError_t side_stream(SideStream** out) {
@@ -1782,8 +1786,11 @@ static cudaError_t side_stream(SideStream** out) {
   SideStream& ss = tab[dev];
   if (ss.s == nullptr) {
     e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ss.h, cudaStreamNonBlocking);
+    cudaEvent_t* evs[] = {&ss.fork, &ss.join, &ss.fork_h, &ss.join_h, &ss.dec[0], &ss.dec[1],
+                          &ss.grp[0], &ss.grp[1], &ss.own[0], &ss.own[1]};
+    for (cudaEvent_t* ev : evs)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
     ss.dev = dev;
   }
@@ -1791,24 +1798,34 @@ static cudaError_t side_stream(SideStream** out) {
   return cudaSuccess;
 }
 
-// Workspace of one SGNS replica: the persistent per-row counters first, then
-// the per-batch buffers.  With base == nullptr only the size is computed.
-struct BatchWs {
-  CorpusDesc* desc;
+// Workspace of one SGNS replica.  The buffers a batch's decode and grouping
+// write come in two halves (by batch parity) so batch i+1 can be decoded and
+// grouped while batch i is still being applied; each half holds persistent
+// per-row counters (zero between batches).  U, G and the coefficients are
+// produced and consumed on the main stream and need one copy.  With
+// base == nullptr only the size is computed.
+struct BatchHalf {
   uint32_t* cnt;
   uint32_t* gctr;
-  void* U;
-  void* G;
-  void* coef;
   int32_t* idx;
   uint32_t* uniq;
   uint32_t* list;
   uint32_t* list_tmp;
   Segment* segs;
   Segment* heavy;
+};
+
+struct BatchWs {
+  CorpusDesc* desc;
+  void* U;
+  void* G;
+  void* coef;
   double* partials;
   void* gsum;
+  BatchHalf half[2];
 };
+
+static bool split_adam_requested() { return getenv("WV_SGNS_SPLIT_ADAM") != nullptr; }
 
 static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, int64_t es, BatchWs& w) {
   const int64_t items = B * (2 + k);
@@ -1818,20 +1835,25 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, in
     off += al256(bytes);
     return p;
   };
+  // the descriptor and the persistent counters sit at offsets that do not
+  // depend on B, so a short final batch sees the same ones
   w.desc = (CorpusDesc*)take(sizeof(CorpusDesc));
-  w.cnt = (uint32_t*)take(2 * V * 4);
-  w.gctr = (uint32_t*)take(64);
+  for (int h = 0; h < 2; ++h) w.half[h].cnt = (uint32_t*)take(2 * V * 4);
   w.U = take(B * d * es);
   w.G = take(B * d * es);
   w.coef = take(B * (k + 1) * es);
-  w.idx = (int32_t*)take(items * 4);
-  w.uniq = (uint32_t*)take(items * 4);
-  w.list = (uint32_t*)take(items * 4);
-  w.list_tmp = (uint32_t*)take(items * 4);
-  w.segs = (Segment*)take(items * (int64_t)sizeof(Segment));
-  w.heavy = (Segment*)take((items / (kLightMax + 1) + 1) * (int64_t)sizeof(Segment));
   w.partials = (double*)take(148 * 32 * 8);
-  w.gsum = take(items * d * es);
+  w.gsum = split_adam_requested() ? take(items * d * es) : nullptr;
+  for (int h = 0; h < 2; ++h) {
+    BatchHalf& x = w.half[h];
+    x.gctr = (uint32_t*)take(64);
+    x.idx = (int32_t*)take(items * 4);
+    x.uniq = (uint32_t*)take(items * 4);
+    x.list = (uint32_t*)take(items * 4);
+    x.list_tmp = (uint32_t*)take(items * 4);
+    x.segs = (Segment*)take(items * (int64_t)sizeof(Segment));
+    x.heavy = (Segment*)take((items / (kLightMax + 1) + 1) * (int64_t)sizeof(Segment));
+  }
   return off + 1024;
 }
 
@@ -2107,7 +2129,7 @@ int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int v
   const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, negatives, batch,
                                       precision == WV_FP64 ? 8 : 4, bw);
   WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
-  WV_CUDA(cudaMemsetAsync(bw.cnt, 0, 2 * vocab_size * 4, (cudaStream_t)stream));
+  for (int h = 0; h < 2; ++h) WV_CUDA(cudaMemsetAsync(bw.half[h].cnt, 0, 2 * vocab_size * 4, (cudaStream_t)stream));
   return 0;
 }
 
@@ -2128,132 +2150,115 @@ int wv_sgns_bind(const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t v
   return 0;
 }
 
-// One SGNS batch: decode -> (gather || grouping) -> owner Adam phase.
-// Every launch is stream-ordered and reads the batch cursor from `state`, so
-// the sequence is CUDA-graph capturable and replayable.
-int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream) {
-  return wv_sgns_batch_phases(model, batch, ws, ws_bytes, WV_PHASE_ALL, stream);
+}  // extern "C"
+
+namespace wv {
+
+// Everything one batch needs, resolved once per call.
+struct BatchCtx {
+  const WvSgnsModel* model;
+  int64_t V, B, items, es;
+  int d, k;
+  BatchWs bw;
+  void* timer;
+  int tb;
+};
+
+static int batch_ctx(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, BatchCtx& c) {
+  c.model = model;
+  c.V = model->vocab_size;
+  c.d = model->vector_size;
+  c.k = batch->negatives;
+  c.B = batch->batch_rows;
+  WV_CHECK_ARG(c.B >= 1, "empty batch");
+  WV_CHECK_ARG(c.k >= 0 && c.k <= 30, "negative_samples must be in [0, 30]");
+  WV_CHECK_ARG(2 * c.V < (int64_t)0xffffffffLL, "vocabulary too large for 32-bit row keys");
+  WV_CHECK_ARG(c.B * (2 + c.k) < (int64_t)0x7fffffffLL, "batch too large");
+  WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
+  c.es = model->precision == WV_FP64 ? 8 : 4;
+  c.items = c.B * (2 + c.k);
+  const int64_t need = carve_batch_ws((char*)ws, c.V, c.d, c.k, c.B, c.es, c.bw);
+  WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
+  c.timer = batch->timer;
+  c.tb = (int)batch->timer_base;
+  return 0;
 }
 
-// The batch split into its phases (PAIRS = decode + gather, GROUP = row
-// grouping, UPDATE = owner Adam) so callers can run them separately; all state
-// flows through the workspace, so calling the phases in order equals one batch.
-int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int phases,
-                         void* stream) {
-  using namespace wv;
-  const int64_t V = model->vocab_size;
-  const int d = model->vector_size;
-  const int k = batch->negatives;
-  const int64_t B = batch->batch_rows;
-  WV_CHECK_ARG(B >= 1, "empty batch");
-  WV_CHECK_ARG(k >= 0 && k <= 30, "negative_samples must be in [0, 30]");
-  WV_CHECK_ARG(2 * V < (int64_t)0xffffffffLL, "vocabulary too large for 32-bit row keys");
-  WV_CHECK_ARG(B * (2 + k) < (int64_t)0xffffffffLL, "batch too large");
-  WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t es = model->precision == WV_FP64 ? 8 : 4;
-  const int64_t items = B * (2 + k);
-  BatchWs bw;
-  const int64_t need = carve_batch_ws((char*)ws, V, d, k, B, es, bw);
-  WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
-  void* U = bw.U;
-  void* G = bw.G;
-  void* coef = bw.coef;
-  int32_t* idx = bw.idx;
-  Segment* segs = bw.segs;
-  Segment* heavy = bw.heavy;
-  double* partials = bw.partials;
-  uint32_t* gctr = bw.gctr;
-  uint32_t* seg_count = gctr + GC_LIGHT;
-
-  {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    WV_CUDA(cudaStreamIsCapturing(st, &cs));
-    if (cs == cudaStreamCaptureStatusNone) {
-      const CorpusDesc c = make_desc(batch);
-      WV_CUDA(cudaMemcpyAsync(bw.desc, &c, sizeof(c), cudaMemcpyHostToDevice, st));
-    }
-  }
+static PairArgs pair_args(const BatchCtx& c, int h) {
   PairArgs pa;
-  pa.V = V;
-  pa.d = d;
-  pa.k = k;
-  pa.B = B;
-  pa.desc = bw.desc;
-  pa.U = U;
-  pa.G = G;
-  pa.coef = coef;
-  pa.cnt = bw.cnt;
-  pa.uniq = bw.uniq;
-  pa.gctr = gctr;
-  pa.idx = idx;
-  pa.partials = partials;
-  pa.state = model->state;
-  const unsigned pgrid = grid_for(B, kPairWarps, 148 * 32);
-  int rc = 0;
-  // PAIRS = decode + gather; GROUP = the grouping sort.  When both are asked
-  // for, the sort runs on a side stream concurrently with the gather.
-  const bool overlap = (phases & WV_PHASE_PAIRS) && (phases & WV_PHASE_GROUP);
-  // optional timestamps (bench/profiling): slots base+0..6 = batch start, decode
-  // end, gather end, join, owner end, sort start, sort end
-  void* timer = batch->timer;
-  const int tb = (int)batch->timer_base;
+  pa.V = c.V;
+  pa.d = c.d;
+  pa.k = c.k;
+  pa.B = c.B;
+  pa.desc = c.bw.desc;
+  pa.U = c.bw.U;
+  pa.G = c.bw.G;
+  pa.coef = c.bw.coef;
+  pa.cnt = c.bw.half[h].cnt;
+  pa.uniq = c.bw.half[h].uniq;
+  pa.gctr = c.bw.half[h].gctr;
+  pa.idx = c.bw.half[h].idx;
+  pa.partials = c.bw.partials;
+  pa.state = c.model->state;
+  return pa;
+}
+
 #define WV_STAMP(slot, strm) \
-  if (timer) WV_CUDA_RC(wv_timer_record(timer, tb + (slot), (void*)(strm)))
-  WV_STAMP(0, st);
-  if (phases & WV_PHASE_PAIRS) {
-    WV_CUDA(cudaMemsetAsync(gctr, 0, 4 * sizeof(uint32_t), st));
-    sgns_decode_kernel<<<grid_for(items, 128, 148 * 32), 128, 0, st>>>(pa);
-    WV_LAUNCH_CHECK();
-  }
-  WV_STAMP(1, st);
-  SideStream* side = nullptr;
-  cudaStream_t sort_st = st;
-  if (overlap) {
-    WV_CUDA(side_stream(&side));
-    WV_CUDA(cudaEventRecord(side->fork, st));
-    WV_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
-    sort_st = side->s;
-  }
-  if (phases & WV_PHASE_GROUP) {
-    WV_STAMP(5, sort_st);
-    group_segments<<<grid_for(items, 256, 148 * 8), 256, 0, sort_st>>>(bw.uniq, bw.cnt, gctr, V, model->sparse,
-                                                                       model->steps_in, model->steps_out, segs,
-                                                                       heavy, items);
-    WV_LAUNCH_CHECK();
-    group_place<<<grid_for(items, 256, 148 * 8), 256, 0, sort_st>>>(idx, B, k, V, bw.cnt, bw.list);
-    WV_LAUNCH_CHECK();
-    WV_STAMP(6, sort_st);
-  }
-  if (phases & WV_PHASE_PAIRS) {
-    rc = dispatch_rows<LaunchPair>(model->precision, d, pa, (const void*)model->input, (const void*)model->output,
-                                   pgrid, st);
-    if (rc) return rc;
-  }
-  WV_STAMP(2, st);
-  if (overlap) {
-    WV_CUDA(cudaEventRecord(side->join, side->s));
-    WV_CUDA(cudaStreamWaitEvent(st, side->join, 0));
-  }
-  WV_STAMP(3, st);
-  if (!(phases & WV_PHASE_UPDATE)) return 0;
+  if (c.timer) WV_CUDA_RC(wv_timer_record(c.timer, c.tb + (slot), (void*)(strm)))
+
+// decode: the batch's row indices + row claims (half h)
+static int enqueue_decode(const BatchCtx& c, int h, cudaStream_t st) {
+  const PairArgs pa = pair_args(c, h);
+  WV_CUDA(cudaMemsetAsync(c.bw.half[h].gctr, 0, 4 * sizeof(uint32_t), st));
+  sgns_decode_kernel<<<grid_for(c.items, 128, 148 * 32), 128, 0, st>>>(pa);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+// grouping: per-row slot lists + RowAdam steps; advances the decode cursor
+static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
+  const BatchHalf& x = c.bw.half[h];
+  const WvSgnsModel* m = c.model;
+  group_segments<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.uniq, x.cnt, x.gctr, c.V, m->sparse, m->steps_in,
+                                                                  m->steps_out, x.segs, x.heavy, c.items, m->state,
+                                                                  c.B);
+  WV_LAUNCH_CHECK();
+  group_place<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.V, x.cnt, x.list);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+static int enqueue_gather(const BatchCtx& c, int h, cudaStream_t st) {
+  const PairArgs pa = pair_args(c, h);
+  const WvSgnsModel* m = c.model;
+  const unsigned pgrid = grid_for(c.B, kPairWarps, 148 * 32);
+  return dispatch_rows<LaunchPair>(m->precision, c.d, pa, (const void*)m->input, (const void*)m->output, pgrid, st);
+}
+
+// owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
+// then (split mode) the Adam pass and (dense mode) the dense Adam sweep
+static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t st) {
+  const WvSgnsModel* model = c.model;
+  const BatchHalf& x = c.bw.half[h];
+  const int64_t V = c.V, B = c.B, items = c.items;
+  const int d = c.d, k = c.k;
   OwnerArgs oa;
   oa.V = V;
   oa.d = d;
   oa.k = k;
   oa.B = B;
   oa.n_items = items;
-  oa.list = bw.list;
-  oa.list_tmp = bw.list_tmp;
-  oa.cnt = bw.cnt;
+  oa.list = x.list;
+  oa.list_tmp = x.list_tmp;
+  oa.cnt = x.cnt;
   oa.slot_bits = bits_for((uint64_t)(items - 1));
   oa.kmag = k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)k + 1ull) : 0xFFFFFFFFu;
-  oa.segs = segs;
-  oa.heavy = heavy;
-  oa.seg_count = seg_count;
-  oa.U = U;
-  oa.G = G;
-  oa.coef = coef;
+  oa.segs = x.segs;
+  oa.heavy = x.heavy;
+  oa.seg_count = x.gctr + GC_LIGHT;
+  oa.U = c.bw.U;
+  oa.G = c.bw.G;
+  oa.coef = c.bw.coef;
   oa.in = model->input;
   oa.out = model->output;
   oa.m_in = model->m_in;
@@ -2268,26 +2273,23 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   oa.sparse = model->sparse;
   oa.dense_g_in = model->dense_g_in;
   oa.dense_g_out = model->dense_g_out;
-  oa.gsum = bw.gsum;
-  oa.split = (model->sparse && getenv("WV_SGNS_SPLIT_ADAM") != nullptr) ? 1 : 0;
+  oa.gsum = c.bw.gsum;
+  oa.split = (model->sparse && c.bw.gsum != nullptr) ? 1 : 0;
   oa.state = model->state;
   const unsigned ogrid = grid_for(items * ((d + 127) / 128), kOwnerThreads / 32, 148 * 32);
-  // heavy rows (side stream) and light rows (main stream) are disjoint: run both at once
-  if (side == nullptr) WV_CUDA(side_stream(&side));
-  WV_CUDA(cudaEventRecord(side->fork, st));
-  WV_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
-  rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 4), side->s);
+  // heavy rows (side) and light rows (main) are disjoint: run both at once
+  WV_CUDA(cudaEventRecord(ss->fork_h, st));
+  WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
+  int rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 4), ss->h);
   if (rc) return rc;
   rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, ogrid, st);
   if (rc) return rc;
-  WV_CUDA(cudaEventRecord(side->join, side->s));
-  WV_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+  WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
+  WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
   if (oa.split) {
     rc = dispatch_rows<LaunchAdam>(model->precision, d, oa, (unsigned)(148 * 16), st);
     if (rc) return rc;
   }
-  WV_STAMP(4, st);
-#undef WV_STAMP
   if (!model->sparse) {
     const int64_t n = V * (int64_t)d;
     if (model->precision == WV_FP32) {
@@ -2309,5 +2311,107 @@ int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, voi
   }
   return 0;
 }
+
+static int bind_if_eager(const WvSgnsBatch* batch, const BatchCtx& c, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  WV_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusNone) {
+    const CorpusDesc d = make_desc(batch);
+    WV_CUDA(cudaMemcpyAsync(c.bw.desc, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+  }
+  return 0;
+}
+
+}  // namespace wv
+
+extern "C" {
+
+// One SGNS batch: decode -> (gather || grouping) -> owner Adam phase.
+// Every launch is stream-ordered and reads the batch cursor from `state`, so
+// the sequence is CUDA-graph capturable and replayable.
+int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream) {
+  return wv_sgns_batch_phases(model, batch, ws, ws_bytes, WV_PHASE_ALL, stream);
+}
+
+// The batch split into its phases (PAIRS = decode + gather, GROUP = row
+// grouping, UPDATE = owner Adam) so callers can run them separately; all state
+// flows through the workspace, so calling the phases in order equals one batch.
+// Uses workspace half 0; optional device timestamps (timer) at: 0 batch start,
+// 1 decode end, 2 gather end, 3 join, 4 owner end, 5 sort start, 6 sort end.
+int wv_sgns_batch_phases(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int phases,
+                         void* stream) {
+  using namespace wv;
+  BatchCtx c;
+  WV_CUDA_RC(batch_ctx(model, batch, ws, ws_bytes, c));
+  cudaStream_t st = (cudaStream_t)stream;
+  WV_CUDA_RC(bind_if_eager(batch, c, st));
+  SideStream* ss = nullptr;
+  WV_CUDA(side_stream(&ss));
+  WV_STAMP(0, st);
+  if (phases & WV_PHASE_PAIRS) WV_CUDA_RC(enqueue_decode(c, 0, st));
+  WV_STAMP(1, st);
+  // when both PAIRS and GROUP are asked for, the grouping runs on the side
+  // stream concurrently with the gather
+  const bool overlap = (phases & WV_PHASE_PAIRS) && (phases & WV_PHASE_GROUP);
+  cudaStream_t sort_st = st;
+  if (overlap) {
+    WV_CUDA(cudaEventRecord(ss->fork, st));
+    WV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    sort_st = ss->s;
+  }
+  if (phases & WV_PHASE_GROUP) {
+    WV_STAMP(5, sort_st);
+    WV_CUDA_RC(enqueue_group(c, 0, sort_st));
+    WV_STAMP(6, sort_st);
+  }
+  if (phases & WV_PHASE_PAIRS) WV_CUDA_RC(enqueue_gather(c, 0, st));
+  WV_STAMP(2, st);
+  if (overlap) {
+    WV_CUDA(cudaEventRecord(ss->join, ss->s));
+    WV_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+  }
+  WV_STAMP(3, st);
+  if (phases & WV_PHASE_UPDATE) WV_CUDA_RC(enqueue_update(c, 0, ss, st));
+  WV_STAMP(4, st);
+  return 0;
+}
+
+// `count` consecutive batches of `batch->batch_rows` pairs, software-pipelined
+// across two workspace halves: the side stream decodes and groups batch i+1
+// while the caller's stream gathers and applies batch i.  Batch i+1's decode
+// waits for batch i-1's update (its half is reused); the gather of batch i+1
+// follows batch i's update on the caller's stream (parameter order), so the
+// result equals `count` calls of wv_sgns_batch.  Capturable as one CUDA graph.
+int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t count,
+                    void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(count >= 1, "count must be >= 1");
+  BatchCtx c;
+  WV_CUDA_RC(batch_ctx(model, batch, ws, ws_bytes, c));
+  c.timer = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  WV_CUDA_RC(bind_if_eager(batch, c, st));
+  SideStream* ss = nullptr;
+  WV_CUDA(side_stream(&ss));
+  WV_CUDA(cudaEventRecord(ss->fork, st));
+  WV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  for (int64_t i = 0; i < count; ++i) {
+    const int h = (int)(i & 1);
+    if (i >= 2) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[h], 0));
+    WV_CUDA_RC(enqueue_decode(c, h, ss->s));
+    WV_CUDA(cudaEventRecord(ss->dec[h], ss->s));
+    WV_CUDA_RC(enqueue_group(c, h, ss->s));
+    WV_CUDA(cudaEventRecord(ss->grp[h], ss->s));
+    WV_CUDA(cudaStreamWaitEvent(st, ss->dec[h], 0));
+    WV_CUDA_RC(enqueue_gather(c, h, st));
+    WV_CUDA(cudaStreamWaitEvent(st, ss->grp[h], 0));
+    WV_CUDA_RC(enqueue_update(c, h, ss, st));
+    WV_CUDA(cudaEventRecord(ss->own[h], st));
+  }
+  WV_CUDA(cudaEventRecord(ss->join, ss->s));
+  WV_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+  return 0;
+}
+#undef WV_STAMP
 
 }  // extern "C"

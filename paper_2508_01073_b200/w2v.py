@@ -416,6 +416,13 @@ class _Replica:
         finally:
             bs.timer, bs.timer_base = None, 0
 
+    def launch_many(self, rows: int, count: int):
+        """``count`` consecutive batches, pipelined across the workspace halves."""
+        bs = self.t.batch_struct
+        bs.batch_rows = int(rows)
+        _lib.call("wv_sgns_batches", C.byref(self.p.struct), C.byref(bs), _lib.ptr(self.ws), self.ws.numel(),
+                  int(count), _lib.stream_ptr())
+
     def _profiled(self, count: int, rows: int, every: int = 16):
         """Eager batches; one in ``every`` bracketed by device timestamps (no graph nodes distort it)."""
         sampled = list(range(0, count, every))
@@ -439,8 +446,7 @@ class _Replica:
             self._profiled(count, rows)
             return
         if G <= 1 or count < 2:
-            for _ in range(count):
-                self.launch(rows)
+            self.launch_many(rows, count)
             return
         key = (rows, min(G, count))
         reps, rem = divmod(count, key[1])
@@ -454,8 +460,7 @@ class _Replica:
             with torch.cuda.stream(cap):
                 g.capture_begin()
                 try:
-                    for _ in range(key[1]):
-                        self.launch(rows)
+                    self.launch_many(rows, key[1])
                 finally:
                     g.capture_end()
             cur.wait_stream(cap)
@@ -466,8 +471,8 @@ class _Replica:
         for _ in range(reps):
             g.replay()
         _lib.note_graph_replay(reps * self.graph_launches[key])
-        for _ in range(rem):
-            self.launch(rows)
+        if rem:
+            self.launch_many(rows, rem)
 
 
 class _Trainer:

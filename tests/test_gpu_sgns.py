@@ -156,3 +156,22 @@ def test_device_mode_loss_tracks_oracle_statistics(wv):
     _, l_dev = wv.train(corpus, V, cfg, 42, pairs="device")
     _, l_np = wv.train(corpus, V, cfg, 42, pairs="numpy")
     assert abs(l_dev[0] - l_np[0]) / l_np[0] < 0.01
+
+
+def test_pipelined_batches_equal_sequential(wv):
+    """wv_sgns_batches (decode/group of batch i+1 overlapping batch i, two workspace
+    halves; CUDA-graph replayed or eager) is bit-identical to one wv_sgns_batch call
+    per batch (the profiled path)."""
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("barabasi", 2000, m=5, predicates=20, seed=3)
+    graph = wv.build_graph(edges, V)
+    corpus = wv.random_walks(graph, ents, walk_depth=4, walk_number=4, rng_seed=9)
+    cfg = wv.TrainConfig(min_count=1, vector_size=24, epochs=1, window_size=3, negative_samples=4, batch_size=997)
+    out = []
+    for graph_batches, profile in ((8, False), (1, False), (8, True)):
+        sess = wv.SkipGramSession(V, cfg, 5, graph_batches=graph_batches)
+        losses = sess.fit(corpus, 2, profile=profile)
+        out.append((sess.model.input_matrix, sess.model.output_matrix, losses))
+    for a in out[1:]:
+        assert np.array_equal(out[0][0], a[0]) and np.array_equal(out[0][1], a[1]) and out[0][2] == a[2]
