@@ -52,6 +52,9 @@ __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(
 __device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
 __device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
 __device__ __forceinline__ float exp_t(float a) { return expf(a); }
+// a*b + c: one FMA for float32; float64 keeps numpy's separate rounding
+__device__ __forceinline__ float mad_t(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double mad_t(double a, double b, double c) { return __dadd_rn(__dmul_rn(a, b), c); }
 __device__ __forceinline__ double exp_t(double a) { return exp(a); }
 
 // ------------------------------------------------------ vector row I/O ----
@@ -278,7 +281,7 @@ struct PairArgs {
 // The list order inside a row is arbitrary; the owner kernels restore slot
 // order (warp ranking / CTA radix sort) before summing, so results are
 // deterministic, and reset cnt[key] to 0 for the next batch.
-enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3 };
+enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3, GC_PIECES = 4 };
 
 __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
   if (atomicAdd(A.cnt + key, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = key;
@@ -418,7 +421,14 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
   }
 }
 
-constexpr int kBulkWarps = 4;
+#ifndef WV_GATHER_WARPS
+#define WV_GATHER_WARPS 8
+#endif
+#ifndef WV_GATHER_STAGES
+#define WV_GATHER_STAGES 2
+#endif
+constexpr int kBulkWarps = WV_GATHER_WARPS;
+constexpr int kBulkStages = WV_GATHER_STAGES;  // pairs in flight per warp
 constexpr int kBulkThreads = kBulkWarps * 32;
 
 // Phase 1b (default path): warp per pair with the 2+k rows fetched by
@@ -437,12 +447,12 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
   const int C = d / EPC;
   const int64_t B = A.B;
   const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [warps][2]
-  T* ring = reinterpret_cast<T*>(smem_raw + 128) + (size_t)warp * 2 * R * d;
-  uint64_t* mybar = bars + 2 * warp;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [warps][kBulkStages]
+  T* ring = reinterpret_cast<T*>(smem_raw + 16 * kBulkWarps * kBulkStages) + (size_t)warp * kBulkStages * R * d;
+  uint64_t* mybar = bars + kBulkStages * warp;
   if (lane == 0) {
-    mbar_init(mybar, 1);
-    mbar_init(mybar + 1, 1);
+#pragma unroll
+    for (int st = 0; st < kBulkStages; ++st) mbar_init(mybar + st, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -452,7 +462,6 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
   const T invB = (T)1 / (T)B;
   const int64_t stride = (int64_t)gridDim.x * kBulkWarps;
   int64_t b = blockIdx.x * (int64_t)kBulkWarps + warp;
-  // prologue: stage 0 <- first pair
   auto issue = [&](int64_t pb, int stage) {
     T* dst = ring + (size_t)stage * R * d;
     int32_t r = 0;
@@ -464,19 +473,22 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
       bulk_row_g2s(dst + (size_t)lane * d, src, row_bytes, mybar + stage);
     }
   };
-  if (b < B) issue(b, 0);
+  // prologue: the first kBulkStages - 1 pairs
+#pragma unroll
+  for (int st = 0; st < kBulkStages - 1; ++st)
+    if (b + st * stride < B) issue(b + st * stride, st);
   double loss_acc = 0.0;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phase = 0u;  // bit per stage
   for (int it = 0; b < B; ++it, b += stride) {
-    const int stage = it & 1;
-    const int64_t nb = b + stride;
+    const int stage = it % kBulkStages;
+    const int64_t nb = b + (int64_t)(kBulkStages - 1) * stride;
     if (nb < B) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(nb, stage ^ 1);
+      issue(nb, (it + kBulkStages - 1) % kBulkStages);
     }
-    while (!mbar_try_wait(mybar + stage, phase[stage])) {
+    while (!mbar_try_wait(mybar + stage, (phase >> stage) & 1u)) {
     }
-    phase[stage] ^= 1u;
+    phase ^= 1u << stage;
     const T* rows = ring + (size_t)stage * R * d;
     Chunk<T, EPC> u[MAXC];
 #pragma unroll
@@ -529,14 +541,14 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
         if (c < C) {
           const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)(1 + j) * d + c * EPC);
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) acc.v[e] = add_rn(acc.v[e], mul_rn(gneg, x.v[e]));
+          for (int e = 0; e < EPC; ++e) acc.v[e] = mad_t(gneg, x.v[e], acc.v[e]);
         }
       }
       if (c < C) {
         const Chunk<T, EPC> v = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)d + c * EPC);
         Chunk<T, EPC> gg;
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) gg.v[e] = add_rn(mul_rn(gpos, v.v[e]), acc.v[e]);
+        for (int e = 0; e < EPC; ++e) gg.v[e] = mad_t(gpos, v.v[e], acc.v[e]);
         st_chunk<T, EPC>(G + b * d + c * EPC, gg);
         st_chunk<T, EPC>(U + b * d + c * EPC, u[q]);
       }
@@ -806,6 +818,65 @@ __global__ void group_place(const int32_t* __restrict__ idx, int64_t B, int k, i
   }
 }
 
+// Contribution slot -> (source U/G row, coefficient index); ci = 0xffffffff
+// marks an input-side contribution (G row, coefficient 1).
+__device__ __forceinline__ uint2 slot_entry(uint32_t v, bool side_out, int64_t B, int k, uint32_t kmag) {
+  if (!side_out) return make_uint2(v, 0xffffffffu);
+  const uint32_t sv = v - (uint32_t)B;
+  uint32_t pp, j;
+  if (sv < (uint32_t)B) {
+    pp = sv;
+    j = 0;
+  } else {
+    const uint32_t t = sv - (uint32_t)B;
+    pp = __umulhi(t, kmag);
+    int32_t r = (int32_t)(t - pp * (uint32_t)k);
+    if (r < 0) {
+      --pp;
+      r += k;
+    } else if (r >= k) {
+      ++pp;
+      r -= k;
+    }
+    j = 1 + (uint32_t)r;
+  }
+  return make_uint2(pp, pp * (uint32_t)(k + 1) + j);
+}
+
+// Light rows only: restore slot order inside each row's list (<= kLightMax
+// entries, insertion sort in registers) and resolve every slot to its source
+// (U/G row, coefficient index), so the owner's per-element threads walk a
+// ready list.  Runs on the side stream with the grouping (off the critical
+// path once batches are pipelined).  ci = 0xffffffff marks an input-side
+// contribution (G row, coefficient 1).
+__global__ void group_order(const Segment* __restrict__ segs, const uint32_t* __restrict__ gctr,
+                            const uint32_t* __restrict__ list, uint2* __restrict__ ents, int64_t V, int64_t B, int k,
+                            uint32_t kmag) {
+  const uint32_t nl = *(volatile const uint32_t*)(gctr + GC_LIGHT);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
+    const Segment sg = segs[i];
+    const bool side_out = sg.key >= (uint32_t)V;
+    uint32_t sl[kLightMax];
+#pragma unroll
+    for (int q = 0; q < kLightMax; ++q) sl[q] = q < (int)sg.len ? list[sg.start + q] : 0xffffffffu;
+    // insertion sort (sentinels sort last)
+#pragma unroll
+    for (int q = 1; q < kLightMax; ++q) {
+#pragma unroll
+      for (int j = q; j > 0; --j) {
+        const uint32_t a = sl[j - 1], b = sl[j];
+        sl[j - 1] = min(a, b);
+        sl[j] = max(a, b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kLightMax; ++q) {
+      if (q >= (int)sg.len) break;
+      ents[sg.start + q] = slot_entry(sl[q], side_out, B, k, kmag);
+    }
+  }
+}
+
 struct OwnerArgs {
   int64_t V;
   int d;
@@ -817,6 +888,8 @@ struct OwnerArgs {
   uint32_t* cnt;         // reset to 0 per row once consumed
   int slot_bits;         // bits of the largest slot (2B + Bk - 1)
   uint32_t kmag;         // ~2^32 / k for the slot -> (pair, negative) split
+  uint32_t cmag;         // ~2^32 / (d / EPC) for the flat owner's (row, chunk) split
+  const uint2* ents;     // light rows: slot-ordered (source row, coefficient index), from group_order
   const Segment* segs;
   const Segment* heavy;
   const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
@@ -1256,6 +1329,109 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
   }
 }
 
+// Phase 3 (default, sparse RowAdam): one thread per kFlatU x (light row,
+// 16-byte chunk) items in a flat grid-stride space, so no lane idles on a row's ragged
+// chunk count and every thread's loads are independent (the access pattern
+// measured closest to HBM bandwidth, profiles/micro/rows_bench.cu).  The
+// row's optimizer state is loaded as soon as its segment record is known;
+// contributions come from group_order's slot-ordered list and are summed in
+// that order (w2v.py:415 np.add.at order), then RowAdam is applied in place.
+#ifndef WV_FLAT_U
+#define WV_FLAT_U 1
+#endif
+#ifndef WV_FLAT_MINB
+#define WV_FLAT_MINB 4
+#endif
+constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
+template <typename T, int EPC>
+__global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(OwnerArgs A) {
+  const int d = A.d;
+  const uint32_t C = (uint32_t)(d / EPC);
+  const uint32_t nseg = *A.seg_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    WvSgnsDevState* st = A.state;
+    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)nseg);
+    st->batch += 1;
+    st->step += 1;
+  }
+  const T* U = (const T*)A.U;
+  const T* G = (const T*)A.G;
+  const T* coef = (const T*)A.coef;
+  const T lr = (T)A.lr;
+  const uint32_t total = nseg * C;
+  const uint32_t stride = gridDim.x * blockDim.x * kFlatU;
+  for (uint32_t i0 = blockIdx.x * blockDim.x * kFlatU + threadIdx.x; i0 < total; i0 += stride) {
+    Segment sg[kFlatU];
+    int32_t cr[kFlatU];
+    bool ok[kFlatU];
+#pragma unroll
+    for (int u = 0; u < kFlatU; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      ok[u] = i < total;
+      uint32_t r = __umulhi(i, A.cmag);
+      cr[u] = (int32_t)(i - r * C);
+      if (cr[u] < 0) {
+        --r;
+        cr[u] += (int32_t)C;
+      } else if (cr[u] >= (int32_t)C) {
+        ++r;
+        cr[u] -= (int32_t)C;
+      }
+      if (ok[u]) sg[u] = A.segs[r];
+    }
+    Chunk<T, EPC> p[kFlatU], m[kFlatU], vv[kFlatU], g[kFlatU];
+#pragma unroll
+    for (int u = 0; u < kFlatU; ++u) {
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) g[u].v[e] = 0;
+      if (!ok[u]) continue;
+      const bool side_out = sg[u].key >= (uint32_t)A.V;
+      const int64_t row = side_out ? (int64_t)sg[u].key - A.V : (int64_t)sg[u].key;
+      const int64_t o = row * d + (int64_t)cr[u] * EPC;
+      p[u] = ld_chunk_rw<T, EPC>((const T*)(side_out ? A.out : A.in) + o);
+      m[u] = ld_chunk_rw<T, EPC>((const T*)(side_out ? A.m_out : A.m_in) + o);
+      vv[u] = ld_chunk_rw<T, EPC>((const T*)(side_out ? A.v_out : A.v_in) + o);
+    }
+#pragma unroll
+    for (int u = 0; u < kFlatU; ++u) {
+      if (!ok[u]) continue;
+      const bool side_out = sg[u].key >= (uint32_t)A.V;
+      const T* srcb = (side_out ? U : G) + (int64_t)cr[u] * EPC;
+      for (uint32_t q = 0; q < sg[u].len; ++q) {
+        const uint2 en = __ldg(A.ents + sg[u].start + q);
+        const Chunk<T, EPC> x = ld_chunk<T, EPC>(srcb + (int64_t)en.x * d);
+        if (side_out) {
+          const T c = __ldg(coef + en.y);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) g[u].v[e] = add_rn(g[u].v[e], mul_rn(c, x.v[e]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) g[u].v[e] = add_rn(g[u].v[e], x.v[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFlatU; ++u) {
+      if (!ok[u]) continue;
+      const bool side_out = sg[u].key >= (uint32_t)A.V;
+      const int64_t row = side_out ? (int64_t)sg[u].key - A.V : (int64_t)sg[u].key;
+      const int64_t o = row * d + (int64_t)cr[u] * EPC;
+      const AdamBC<T> bc(sg[u].bc1, sg[u].bc2);
+      bool changed = false;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p[u].v[e], m[u].v[e], vv[u].v[e], g[u].v[e], bc, lr) != T(0);
+      st_chunk<T, EPC>((T*)(side_out ? A.out : A.in) + o, p[u]);
+      st_chunk<T, EPC>((T*)(side_out ? A.m_out : A.m_in) + o, m[u]);
+      st_chunk<T, EPC>((T*)(side_out ? A.v_out : A.v_in) + o, vv[u]);
+      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+      if (cr[u] == 0) {
+        (side_out ? A.touched_out : A.touched_in)[row] = 1;
+        A.cnt[sg[u].key] = 0;
+      }
+    }
+  }
+}
+
 // Stable LSD radix sort (8-bit digits) of n slots by one CTA of kHeavyThreads
 // threads: a ping-pongs with tmp; returns the buffer holding the result.  Per
 // tile of kHeavyThreads items each warp ranks equal digits with match_any and
@@ -1324,7 +1500,16 @@ __device__ uint32_t* cta_sort_slots(uint32_t* a, uint32_t* tmp, uint32_t n, int 
 // in part order through shared memory (a fixed two-level order, so the result
 // is deterministic), then the threads apply RowAdam element-parallel.
 template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) {
+#ifndef WV_HEAVY_MINB
+#define WV_HEAVY_MINB 1
+#endif
+#ifndef WV_HEAVY_GRID
+#define WV_HEAVY_GRID (148 * 4)
+#endif
+#ifndef WV_OWNER_PER_SM
+#define WV_OWNER_PER_SM 0  // 0: all resident CTAs
+#endif
+__global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kernel(OwnerArgs A) {
   constexpr int W = kHeavyThreads / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* part = reinterpret_cast<T*>(smem_raw);  // [W][d]
@@ -1465,6 +1650,193 @@ __global__ void __launch_bounds__(kHeavyThreads) sgns_heavy_kernel(OwnerArgs A) 
       A.cnt[key] = 0;
     }
     __syncthreads();  // shared buffers are reused by the next heavy row
+  }
+}
+
+// ------------------------------------------------ heavy rows, split -----
+// Heavy rows (predicates, hub entities: > kLightMax contributions, up to
+// thousands) are spread over many warps instead of one CTA per row, so the
+// hottest row no longer bounds the phase: heavy_order (side stream, off the
+// critical path) sorts each heavy row's list into slot order, resolves the
+// entries and cuts the row into pieces of kPiece contributions; heavy_piece
+// (one warp per piece) sums its piece in slot order, and the warp finishing a
+// row's last piece sums the piece partials in piece order and applies RowAdam.
+// The association ((c0 + .. + c31) + (c32 + ..)) is fixed, so results are
+// deterministic run to run.
+constexpr int kPiece = 32;
+
+__host__ __device__ __forceinline__ int64_t max_pieces(int64_t items) {
+  return items / kPiece + items / (kLightMax + 1) + 2;
+}
+
+__global__ void __launch_bounds__(kHeavyThreads) heavy_order(OwnerArgs A, uint32_t* gctr, uint2* pieces) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem_raw);
+  const uint32_t bitmap_words = heavy_bitmap_words(A.n_items);
+  __shared__ uint32_t sort_hist[kHeavyThreads / 32][256];
+  __shared__ uint32_t s_pbase;
+  const uint32_t nh = *(volatile uint32_t*)(gctr + GC_HEAVY);
+  Segment* heavy = const_cast<Segment*>(A.heavy);
+  uint2* ents = const_cast<uint2*>(A.ents);
+  for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const Segment sg = heavy[h];
+    const bool side_out = sg.key >= (uint32_t)A.V;
+    const uint32_t* sorted;
+    if (bitmap_words > 0) {
+      for (uint32_t i = threadIdx.x; i < bitmap_words; i += kHeavyThreads) bitmap[i] = 0u;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads) {
+        const uint32_t x = A.list[sg.start + i];
+        atomicOr(&bitmap[x >> 5], 1u << (x & 31));
+      }
+      __syncthreads();
+      const uint32_t per_t = (bitmap_words + kHeavyThreads - 1) / kHeavyThreads;
+      const uint32_t w0 = min(bitmap_words, threadIdx.x * per_t), w1 = min(bitmap_words, w0 + per_t);
+      uint32_t mine = 0;
+      for (uint32_t w = w0; w < w1; ++w) mine += __popc(bitmap[w]);
+      __shared__ uint32_t scan_total;
+      uint32_t pos = block_excl_scan<uint32_t, kHeavyThreads>(mine, &scan_total);
+      uint32_t* out_sorted = A.list_tmp + sg.start;
+      for (uint32_t w = w0; w < w1; ++w) {
+        uint32_t bits = bitmap[w];
+        while (bits) {
+          const int bt = __ffs(bits) - 1;
+          out_sorted[pos++] = w * 32u + (uint32_t)bt;
+          bits &= bits - 1u;
+        }
+      }
+      __syncthreads();
+      sorted = out_sorted;
+    } else {
+      sorted = cta_sort_slots(const_cast<uint32_t*>(A.list) + sg.start, A.list_tmp + sg.start, sg.len, A.slot_bits,
+                              sort_hist);
+    }
+    for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads)
+      ents[sg.start + i] = slot_entry(sorted[i], side_out, A.B, A.k, A.kmag);
+    const uint32_t np = (sg.len + kPiece - 1) / kPiece;
+    if (threadIdx.x == 0) {
+      s_pbase = atomicAdd(gctr + GC_PIECES, np);
+      heavy[h].pad = s_pbase;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < np; j += kHeavyThreads) pieces[s_pbase + j] = make_uint2(h, j);
+    __syncthreads();  // shared buffers are reused by the next heavy row
+  }
+}
+
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* gctr, const uint2* pieces,
+                                                   T* partial, uint32_t* rowdone) {
+  const int lane = threadIdx.x & 31;
+  const int d = A.d;
+  const int C = d / EPC;
+  const uint32_t np_total = *(volatile const uint32_t*)(gctr + GC_PIECES);
+  const T* U = (const T*)A.U;
+  const T* G = (const T*)A.G;
+  const T* coef = (const T*)A.coef;
+  const T lr = (T)A.lr;
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd((unsigned long long*)&A.state->rows_updated, (unsigned long long)gctr[GC_HEAVY]);
+  for (uint32_t pc = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); pc < np_total; pc += warps) {
+    const uint2 pd = pieces[pc];
+    const Segment sg = A.heavy[pd.x];
+    const bool side_out = sg.key >= (uint32_t)A.V;
+    const uint32_t np = (sg.len + kPiece - 1) / kPiece;
+    const uint32_t q0 = pd.y * kPiece;
+    const int n = (int)min((uint32_t)kPiece, sg.len - q0);
+    uint2 my = make_uint2(0, 0);
+    T my_c = 1;
+    if (lane < n) {
+      my = __ldg(A.ents + sg.start + q0 + lane);
+      if (side_out) my_c = __ldg(coef + my.y);
+    }
+    const T* srcb = side_out ? U : G;
+    Chunk<T, EPC> g[MAXC];
+#pragma unroll
+    for (int qq = 0; qq < MAXC; ++qq)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) g[qq].v[e] = 0;
+    for (int j0 = 0; j0 < n; j0 += 8) {
+      uint32_t ri[8];
+      T c[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        ri[q] = __shfl_sync(0xffffffffu, my.x, (j0 + q) & 31);
+        c[q] = __shfl_sync(0xffffffffu, my_c, (j0 + q) & 31);
+      }
+#pragma unroll
+      for (int qq = 0; qq < MAXC; ++qq) {
+        const int cc = lane + 32 * qq;
+        if (cc < C) {
+          Chunk<T, EPC> x[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (j0 + q < n) x[q] = ld_chunk<T, EPC>(srcb + (size_t)ri[q] * d + cc * EPC);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (j0 + q < n) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e)
+                g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(c[q], x[q].v[e]) : x[q].v[e]);
+            }
+        }
+      }
+    }
+    if (np > 1) {
+      // publish the piece partial; the warp finishing the row's last piece applies it
+#pragma unroll
+      for (int qq = 0; qq < MAXC; ++qq) {
+        const int cc = lane + 32 * qq;
+        if (cc < C) st_chunk<T, EPC>(partial + ((size_t)sg.pad + pd.y) * d + cc * EPC, g[qq]);
+      }
+      __threadfence();
+      __syncwarp();
+      uint32_t last = 0;
+      if (lane == 0) last = atomicAdd(rowdone + pd.x, 1u) == np - 1 ? 1u : 0u;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (!last) continue;
+      __threadfence();
+#pragma unroll
+      for (int qq = 0; qq < MAXC; ++qq) {
+        const int cc = lane + 32 * qq;
+        if (cc < C) {
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) g[qq].v[e] = 0;
+          for (uint32_t t = 0; t < np; ++t) {
+            const T* src = partial + ((size_t)sg.pad + t) * d + cc * EPC;
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) g[qq].v[e] = add_rn(g[qq].v[e], __ldcg(src + e));
+          }
+        }
+      }
+      if (lane == 0) rowdone[pd.x] = 0;
+    }
+    const int64_t row = side_out ? (int64_t)sg.key - A.V : (int64_t)sg.key;
+    T* P = (T*)(side_out ? A.out : A.in);
+    T* M = (T*)(side_out ? A.m_out : A.m_in);
+    T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    const AdamBC<T> bc(sg.bc1, sg.bc2);
+    bool changed = false;
+#pragma unroll
+    for (int qq = 0; qq < MAXC; ++qq) {
+      const int cc = lane + 32 * qq;
+      if (cc < C) {
+        const int64_t o = row * d + (int64_t)cc * EPC;
+        Chunk<T, EPC> p = ld_chunk_rw<T, EPC>(P + o), m = ld_chunk_rw<T, EPC>(M + o), vv = ld_chunk_rw<T, EPC>(Vv + o);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g[qq].v[e], bc, lr) != T(0);
+        st_chunk<T, EPC>(P + o, p);
+        st_chunk<T, EPC>(M + o, m);
+        st_chunk<T, EPC>(Vv + o, vv);
+      }
+    }
+    changed = __any_sync(0xffffffffu, changed);
+    if (lane == 0) {
+      (side_out ? A.touched_out : A.touched_in)[row] = 1;
+      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+      A.cnt[sg.key] = 0;
+    }
   }
 }
 
@@ -1718,9 +2090,9 @@ static int dispatch_rows(int precision, int d, Args&&... args) {
 
 // shared memory of the bulk gather: barriers + per-warp two-stage ring of 2+k rows
 static inline size_t bulk_smem_bytes(int d, int k, size_t es) {
-  return 128 + (size_t)kBulkWarps * 2 * (2 + k) * d * es;
+  return 16 * kBulkWarps * kBulkStages + (size_t)kBulkWarps * kBulkStages * (2 + k) * d * es;
 }
-static constexpr size_t kBulkSmemMax = 112 * 1024;  // two CTAs per SM
+static constexpr size_t kBulkSmemMax = 220 * 1024;
 
 template <typename T, int EPC, int MAXC>
 struct LaunchPair {
@@ -1731,13 +2103,13 @@ struct LaunchPair {
     const bool bulk = (a.d * sizeof(T)) % 16 == 0 && EPC * sizeof(T) == 16 && smem <= kBulkSmemMax &&
                       getenv("WV_SGNS_REG_GATHER") == nullptr;
     if (bulk) {
-      static bool attr_set[16] = {false};
+      static size_t attr_set[16] = {0};
       int dev = 0;
       cudaGetDevice(&dev);
-      if (dev >= 0 && dev < 16 && !attr_set[dev]) {
+      if (dev >= 0 && dev < 16 && attr_set[dev] < smem) {
         WV_CUDA(cudaFuncSetAttribute(sgns_gather_bulk_kernel<T, EPC, MAXC>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmemMax));
-        attr_set[dev] = true;
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set[dev] = smem;
       }
       // persistent grid: exactly the resident CTAs (no partial second wave)
       static int resident[16] = {0};
@@ -1813,6 +2185,10 @@ struct BatchHalf {
   uint32_t* list_tmp;
   Segment* segs;
   Segment* heavy;
+  uint2* ents;
+  uint2* pieces;     // heavy-row pieces (row, piece index)
+  void* partial;     // [max_pieces, d] piece partial sums
+  uint32_t* rowdone; // per heavy row: pieces finished (zero between batches)
 };
 
 struct BatchWs {
@@ -1853,6 +2229,10 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, in
     x.list_tmp = (uint32_t*)take(items * 4);
     x.segs = (Segment*)take(items * (int64_t)sizeof(Segment));
     x.heavy = (Segment*)take((items / (kLightMax + 1) + 1) * (int64_t)sizeof(Segment));
+    x.ents = (uint2*)take(items * 8);
+    x.pieces = (uint2*)take(max_pieces(items) * 8);
+    x.partial = take(max_pieces(items) * d * es);
+    x.rowdone = (uint32_t*)take((items / (kLightMax + 1) + 1) * 4);  // zeroed per batch with gctr
   }
   return off + 1024;
 }
@@ -1908,7 +2288,30 @@ struct LaunchHeavy {
 
 template <typename T, int EPC, int MAXC>
 struct LaunchOwner {
-  static int run(const OwnerArgs& a, unsigned grid, cudaStream_t st) {
+  static int run(const OwnerArgs& a0, unsigned grid, cudaStream_t st) {
+    OwnerArgs a = a0;
+    if (a.ents != nullptr) {  // flat owner (group_order ran): persistent grid of resident CTAs
+      const uint32_t C = (uint32_t)(a.d / EPC);
+      a.cmag = C > 1 ? (uint32_t)(0xFFFFFFFFull / C + 1ull) : 0xFFFFFFFFu;
+      static int resident[16] = {0};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      int sms = 148;
+      if (dev >= 0 && dev < 16) {
+        if (resident[dev] == 0) {
+          int nb = 0;
+          WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_owner_flat_kernel<T, EPC>, 256, 0));
+          resident[dev] = nb > 0 ? nb : 1;
+        }
+        WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      int per = dev >= 0 && dev < 16 ? resident[dev] : 4;
+      if (WV_OWNER_PER_SM > 0 && per > WV_OWNER_PER_SM) per = WV_OWNER_PER_SM;
+      const unsigned g = (unsigned)(sms * per);
+      sgns_owner_flat_kernel<T, EPC><<<g, 256, 0, st>>>(a);
+      WV_LAUNCH_CHECK();
+      return 0;
+    }
     const size_t smem = 128 + (size_t)kOwnerBulkWarps * 2 * kOwnerBulkRows * a.d * sizeof(T);
     if (a.sparse && !a.split && (a.d * sizeof(T)) % 16 == 0 && EPC * sizeof(T) == 16 && smem <= 112 * 1024 &&
         getenv("WV_SGNS_REG_OWNER") == nullptr) {
@@ -2206,53 +2609,41 @@ static PairArgs pair_args(const BatchCtx& c, int h) {
 #define WV_STAMP(slot, strm) \
   if (c.timer) WV_CUDA_RC(wv_timer_record(c.timer, c.tb + (slot), (void*)(strm)))
 
+// the flat per-element owner serves sparse RowAdam (default); the warp-per-row
+// kernels remain for dense mode, split mode and WV_SGNS_BULK_OWNER=1
+static bool flat_owner(const BatchCtx& c) {
+  return c.model->sparse && c.bw.gsum == nullptr && getenv("WV_SGNS_BULK_OWNER") == nullptr;
+}
+
 // decode: the batch's row indices + row claims (half h)
 static int enqueue_decode(const BatchCtx& c, int h, cudaStream_t st) {
   const PairArgs pa = pair_args(c, h);
-  WV_CUDA(cudaMemsetAsync(c.bw.half[h].gctr, 0, 4 * sizeof(uint32_t), st));
+  WV_CUDA(cudaMemsetAsync(c.bw.half[h].gctr, 0, 8 * sizeof(uint32_t), st));
+  if (flat_owner(c))
+    WV_CUDA(cudaMemsetAsync(c.bw.half[h].rowdone, 0, (c.items / (kLightMax + 1) + 1) * 4, st));
   sgns_decode_kernel<<<grid_for(c.items, 128, 148 * 32), 128, 0, st>>>(pa);
   WV_LAUNCH_CHECK();
   return 0;
 }
 
-// grouping: per-row slot lists + RowAdam steps; advances the decode cursor
-static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
-  const BatchHalf& x = c.bw.half[h];
-  const WvSgnsModel* m = c.model;
-  group_segments<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.uniq, x.cnt, x.gctr, c.V, m->sparse, m->steps_in,
-                                                                  m->steps_out, x.segs, x.heavy, c.items, m->state,
-                                                                  c.B);
-  WV_LAUNCH_CHECK();
-  group_place<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.V, x.cnt, x.list);
-  WV_LAUNCH_CHECK();
-  return 0;
-}
-
-static int enqueue_gather(const BatchCtx& c, int h, cudaStream_t st) {
-  const PairArgs pa = pair_args(c, h);
-  const WvSgnsModel* m = c.model;
-  const unsigned pgrid = grid_for(c.B, kPairWarps, 148 * 32);
-  return dispatch_rows<LaunchPair>(m->precision, c.d, pa, (const void*)m->input, (const void*)m->output, pgrid, st);
-}
-
-// owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
-// then (split mode) the Adam pass and (dense mode) the dense Adam sweep
-static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t st) {
+static OwnerArgs owner_args(const BatchCtx& c, int h) {
   const WvSgnsModel* model = c.model;
   const BatchHalf& x = c.bw.half[h];
-  const int64_t V = c.V, B = c.B, items = c.items;
-  const int d = c.d, k = c.k;
+  const int64_t items = c.items;
+  const int k = c.k;
   OwnerArgs oa;
-  oa.V = V;
-  oa.d = d;
+  oa.V = c.V;
+  oa.d = c.d;
   oa.k = k;
-  oa.B = B;
+  oa.B = c.B;
   oa.n_items = items;
   oa.list = x.list;
   oa.list_tmp = x.list_tmp;
   oa.cnt = x.cnt;
   oa.slot_bits = bits_for((uint64_t)(items - 1));
   oa.kmag = k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)k + 1ull) : 0xFFFFFFFFu;
+  oa.cmag = 0;
+  oa.ents = flat_owner(c) ? x.ents : nullptr;
   oa.segs = x.segs;
   oa.heavy = x.heavy;
   oa.seg_count = x.gctr + GC_LIGHT;
@@ -2276,11 +2667,80 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
   oa.gsum = c.bw.gsum;
   oa.split = (model->sparse && c.bw.gsum != nullptr) ? 1 : 0;
   oa.state = model->state;
+  return oa;
+}
+
+// grouping: per-row slot lists + RowAdam steps; advances the decode cursor
+static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
+  const BatchHalf& x = c.bw.half[h];
+  const WvSgnsModel* m = c.model;
+  group_segments<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.uniq, x.cnt, x.gctr, c.V, m->sparse, m->steps_in,
+                                                                  m->steps_out, x.segs, x.heavy, c.items, m->state,
+                                                                  c.B);
+  WV_LAUNCH_CHECK();
+  group_place<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.V, x.cnt, x.list);
+  WV_LAUNCH_CHECK();
+  if (flat_owner(c)) {
+    const uint32_t kmag = c.k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)c.k + 1ull) : 0xFFFFFFFFu;
+    group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, kmag);
+    WV_LAUNCH_CHECK();
+    OwnerArgs oa = owner_args(c, h);
+    const size_t smem = (size_t)heavy_bitmap_words(c.items) * 4;
+    static size_t attr[16] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 16 && attr[dev] < smem) {
+      WV_CUDA(cudaFuncSetAttribute(heavy_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr[dev] = smem;
+    }
+    heavy_order<<<148 * 2, kHeavyThreads, smem, st>>>(oa, x.gctr, x.pieces);
+    WV_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+static int enqueue_gather(const BatchCtx& c, int h, cudaStream_t st) {
+  const PairArgs pa = pair_args(c, h);
+  const WvSgnsModel* m = c.model;
+  const unsigned pgrid = grid_for(c.B, kPairWarps, 148 * 32);
+  return dispatch_rows<LaunchPair>(m->precision, c.d, pa, (const void*)m->input, (const void*)m->output, pgrid, st);
+}
+
+// owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
+// then (split mode) the Adam pass and (dense mode) the dense Adam sweep
+template <typename T, int EPC, int MAXC>
+struct LaunchPieces {
+  static int run(const OwnerArgs& a, const BatchHalf& x, cudaStream_t st) {
+    heavy_piece<T, EPC, MAXC><<<148 * 2, 256, 0, st>>>(a, x.gctr, x.pieces, (T*)x.partial, x.rowdone);
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+};
+
+// owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
+// then (split mode) the Adam pass and (dense mode) the dense Adam sweep
+static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t st) {
+  const WvSgnsModel* model = c.model;
+  const int64_t V = c.V, items = c.items;
+  const int d = c.d;
+  const OwnerArgs oa = owner_args(c, h);
+  if (flat_owner(c)) {
+    // heavy pieces (few warps, short) first on the side stream, then the flat light-row owner
+    WV_CUDA(cudaEventRecord(ss->fork_h, st));
+    WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
+    int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, c.bw.half[h], ss->h);
+    if (rc) return rc;
+    rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
+    if (rc) return rc;
+    WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
+    WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
+    return 0;
+  }
   const unsigned ogrid = grid_for(items * ((d + 127) / 128), kOwnerThreads / 32, 148 * 32);
   // heavy rows (side) and light rows (main) are disjoint: run both at once
   WV_CUDA(cudaEventRecord(ss->fork_h, st));
   WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
-  int rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(148 * 4), ss->h);
+  int rc = dispatch_rows<LaunchHeavy>(model->precision, d, oa, (unsigned)(WV_HEAVY_GRID), ss->h);
   if (rc) return rc;
   rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, ogrid, st);
   if (rc) return rc;
