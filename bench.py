@@ -236,37 +236,79 @@ def host_csr(g):
 
 
 # ------------------------------------------------------------- reference ----
+_REF = {}  # inherited by forked reference workers (CSR, roots, initial state)
+
+
+def _ref_worker(job):
+    """One reference worker: its own replica (init + RowAdam + negative stream, as a
+    _train_multi worker, w2v.py:579-746) over its own walk shards."""
+    wid, n_workers, warmup, steps, batches = job
+    from oracle import w2v as ow2v
+
+    inp, out = _REF["init"]  # forked: the replica's pages are copied on first write
+    state = {"inp": inp, "out": out, "ai": ow2v.RowAdam(inp.shape, LR), "ao": ow2v.RowAdam(out.shape, LR),
+             "rng": np.random.default_rng(np.random.SeedSequence([SEED, 1, 2, wid]))}
+    rows = []
+    for i in range(warmup + steps):
+        shard = (i * n_workers + wid) % _REF["n_shards"]
+        res, state = cpu_sample(_REF["off"], _REF["tgt"], _REF["prd"], _REF["roots"], _REF["V"], [shard], batches, state)
+        if i >= warmup:
+            rows.append((res["pipeline_s"], res["pairs_trained"], res["hops"], res["walk_s"]))
+    return rows
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference on the host cores (rank 0 only)."""
+    """--impl reference: the oracle port of the reference on all host cores (rank 0 only).
+
+    One forked worker per core, each a replica of the reference's multi-worker
+    trainer (own Adam state and negative stream, w2v.py:579-746) walking its own
+    8192-walk shards (walks.py:168-173) and training reference batches from them;
+    the replica merge every 64 batches (_merge_bundles) is not timed.  value =
+    pairs trained by all workers / the slowest worker's time.
+    """
     if rank != 0:
         return
+    import multiprocessing as mp
+
     import torch
+
+    from oracle import w2v as ow2v
 
     g, V, ents = make_graph()  # synthetic input only; the timed path below is pure numpy
     off, tgt, prd = host_csr(g)
     roots_np = ents.cpu().numpy()
     del g
     torch.cuda.empty_cache()
-    state = None
-    n_shards = -(-len(roots_np) * WALKS // 8192)
-    times, trained, hops, walk_s = [], 0, 0, 0.0
-    for i in range(args.warmup + args.steps):
-        res, state = cpu_sample(off, tgt, prd, roots_np, V, [i % n_shards], args.ref_batches, state)
-        if i >= args.warmup:
-            times.append(res["pipeline_s"])
-            trained += res["pairs_trained"]
-            hops += res["hops"]
-            walk_s += res["walk_s"]
-    tot = sum(times)
+    # one replica per core; each holds its own parameters + Adam state (~10.5 GB at cfg2 once its
+    # touched pages are copied), so the worker count is also capped by 60% of the available RAM
+    try:
+        import psutil
+
+        mem_cap = max(1, int(0.6 * psutil.virtual_memory().available / 10.5e9))
+    except ImportError:
+        mem_cap = 8
+    cores = int(args.ref_cores) if args.ref_cores else min(len(os.sched_getaffinity(0)), mem_cap)
+    _REF.update(off=off, tgt=tgt, prd=prd, roots=roots_np, V=V, n_shards=-(-len(roots_np) * WALKS // 8192),
+                init=ow2v.init(V, DIM, SEED))
+    jobs = [(w, cores, args.warmup, args.steps, args.ref_batches) for w in range(cores)]
+    with mp.get_context("fork").Pool(cores) as pool:
+        results = pool.map(_ref_worker, jobs)
+    per_worker_s = [sum(r[0] for r in rows) for rows in results]
+    trained = sum(r[1] for rows in results for r in rows)
+    hops = sum(r[2] for rows in results for r in rows)
+    walk_s = max(sum(r[3] for r in rows) for rows in results)
+    tot = max(per_worker_s)
     value = trained / tot
-    sample = (f"per step: one 8192-walk shard of the cfg2 corpus (oracle walks) + {args.ref_batches} SGNS batches of "
-              f"23,933 pairs from its pairs (oracle fp64 numpy); walk/pair-generation time scaled to the trained share")
+    sample = (f"{cores} forked workers (one per host core), each per step: one 8192-walk shard of the cfg2 corpus "
+              f"(oracle walks) + {args.ref_batches} SGNS batches of 23,933 pairs from its pairs (oracle fp64 numpy, "
+              f"own replica as in _train_multi; merge not timed); walk/pair time scaled to the trained share; "
+              f"value = all pairs / slowest worker")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args.roots),
         "walk_hops_per_s": hops / walk_s if walk_s else None,
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -418,7 +460,8 @@ def run_ours(args, rank, world, local):
         "sgns_gather": {"ms": ph.get("gather", float("nan")), "bytes": pair_bytes, "per_step": per},
         "sgns_grouping(side stream, overlaps gather)": {"ms": ph.get("group", float("nan")), "bytes": None,
                                                          "per_step": per},
-        "sgns_owner_adam": {"ms": ph.get("owner", float("nan")), "bytes": owner_bytes, "per_step": per},
+        "sgns_owner_adam(flat light rows + heavy pieces)": {"ms": ph.get("owner", float("nan")), "bytes": owner_bytes,
+                                                            "per_step": per},
     }
     for k_, v_ in kern.items():
         v_["share_of_step"] = v_["ms"] * v_["per_step"] / (ms / args.steps)
@@ -427,9 +470,18 @@ def run_ours(args, rank, world, local):
     dom = max((k_ for k_ in kern if kern[k_]["bytes"]), key=lambda k_: kern[k_]["share_of_step"])
     batch_bytes = pair_bytes + owner_bytes
     batch_ms = ph.get("batch", float("nan"))
+    # ncu DRAM traffic per launch of the owner phase's kernels (same batch geometry), newest capture
+    traffic, traffic_src = None, None
+    tfs = sorted((ROOT / "profiles").glob("traffic_*.json"))
+    if tfs:
+        t_ = json.loads(tfs[-1].read_text())
+        parts = [k_ for k_ in ("sgns_owner_flat", "heavy_piece") if k_ in t_]
+        if parts:
+            traffic = sum(t_[k_]["dram_bytes"] for k_ in parts)
+            traffic_src = f"{tfs[-1].relative_to(ROOT)}: ncu --set full dram__bytes_read+write of {' + '.join(parts)}"
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
-        "frac": kern[dom]["frac"], "traffic": None, "peak_source": peak_src,
+        "frac": kern[dom]["frac"], "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
         "algorithmic_bytes_per_launch": kern[dom]["bytes"], "avg_launch_ms": kern[dom]["ms"],
         "kernels": kern,
         "sgns_batch": {"bytes": batch_bytes, "ms": batch_ms, "gbs": batch_bytes / (batch_ms * 1e-3) / 1e9,
@@ -485,6 +537,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-batches", type=int, default=2, help="SGNS batches per CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-cores", type=int, default=0, help="reference-arm workers (default: all host cores)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

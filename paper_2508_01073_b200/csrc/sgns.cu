@@ -889,7 +889,11 @@ struct OwnerArgs {
   int slot_bits;         // bits of the largest slot (2B + Bk - 1)
   uint32_t kmag;         // ~2^32 / k for the slot -> (pair, negative) split
   uint32_t cmag;         // ~2^32 / (d / EPC) for the flat owner's (row, chunk) split
-  const uint2* ents;     // light rows: slot-ordered (source row, coefficient index), from group_order
+  const uint2* ents;     // slot-ordered (source row, coefficient index), from group_order / heavy_order
+  const uint2* pieces;   // heavy-row pieces (row, piece index) from heavy_order
+  void* partial;         // [pieces, d] piece partial sums
+  uint32_t* rowdone;     // per heavy row: pieces finished (zeroed per batch)
+  const uint32_t* gctr;  // grouping counters (GC_PIECES: piece count)
   const Segment* segs;
   const Segment* heavy;
   const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
@@ -1342,17 +1346,36 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
 #ifndef WV_FLAT_MINB
 #define WV_FLAT_MINB 4
 #endif
+#ifndef WV_OWNER_FUSED_HEAVY
+#define WV_OWNER_FUSED_HEAVY 0
+#endif
+#ifndef WV_PIECE_THREADS
+#define WV_PIECE_THREADS 128
+#endif
+#ifndef WV_PIECE_GRID
+#define WV_PIECE_GRID 148
+#endif
 constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
-template <typename T, int EPC>
+template <typename T, int EPC, int MAXC>
+__device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc);
+template <typename T, int EPC, int MAXC>
 __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(OwnerArgs A) {
   const int d = A.d;
   const uint32_t C = (uint32_t)(d / EPC);
   const uint32_t nseg = *A.seg_count;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     WvSgnsDevState* st = A.state;
-    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)nseg);
+    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)(nseg + A.gctr[GC_HEAVY]));
     st->batch += 1;
     st->step += 1;
+  }
+  // heavy-row pieces first (warp per piece, spread over every SM), then the
+  // light rows' (row, chunk) items
+  if (WV_OWNER_FUSED_HEAVY) {
+    const uint32_t np_total = *(volatile const uint32_t*)(A.gctr + GC_PIECES);
+    const uint32_t warps = gridDim.x * (blockDim.x / 32);
+    for (uint32_t pc = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); pc < np_total; pc += warps)
+      heavy_piece_work<T, EPC, MAXC>(A, pc);
   }
   const T* U = (const T*)A.U;
   const T* G = (const T*)A.G;
@@ -1507,7 +1530,7 @@ template <typename T, int EPC, int MAXC>
 #define WV_HEAVY_GRID (148 * 4)
 #endif
 #ifndef WV_OWNER_PER_SM
-#define WV_OWNER_PER_SM 0  // 0: all resident CTAs
+#define WV_OWNER_PER_SM 3  // light-row owner CTAs per SM (room for the concurrent heavy pieces); 0: all resident
 #endif
 __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kernel(OwnerArgs A) {
   constexpr int W = kHeavyThreads / 32;
@@ -1724,22 +1747,21 @@ __global__ void __launch_bounds__(kHeavyThreads) heavy_order(OwnerArgs A, uint32
   }
 }
 
+constexpr int kPieceGroup = 4;  // contribution rows loaded together per warp
+
+// One heavy-row piece, by one warp (called from the flat owner kernel).
 template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* gctr, const uint2* pieces,
-                                                   T* partial, uint32_t* rowdone) {
+__device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc) {
   const int lane = threadIdx.x & 31;
   const int d = A.d;
   const int C = d / EPC;
-  const uint32_t np_total = *(volatile const uint32_t*)(gctr + GC_PIECES);
   const T* U = (const T*)A.U;
   const T* G = (const T*)A.G;
   const T* coef = (const T*)A.coef;
   const T lr = (T)A.lr;
-  const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd((unsigned long long*)&A.state->rows_updated, (unsigned long long)gctr[GC_HEAVY]);
-  for (uint32_t pc = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); pc < np_total; pc += warps) {
-    const uint2 pd = pieces[pc];
+  T* partial = (T*)A.partial;
+  {
+    const uint2 pd = A.pieces[pc];
     const Segment sg = A.heavy[pd.x];
     const bool side_out = sg.key >= (uint32_t)A.V;
     const uint32_t np = (sg.len + kPiece - 1) / kPiece;
@@ -1757,11 +1779,11 @@ __global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* 
     for (int qq = 0; qq < MAXC; ++qq)
 #pragma unroll
       for (int e = 0; e < EPC; ++e) g[qq].v[e] = 0;
-    for (int j0 = 0; j0 < n; j0 += 8) {
-      uint32_t ri[8];
-      T c[8];
+    for (int j0 = 0; j0 < n; j0 += kPieceGroup) {
+      uint32_t ri[kPieceGroup];
+      T c[kPieceGroup];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < kPieceGroup; ++q) {
         ri[q] = __shfl_sync(0xffffffffu, my.x, (j0 + q) & 31);
         c[q] = __shfl_sync(0xffffffffu, my_c, (j0 + q) & 31);
       }
@@ -1769,12 +1791,12 @@ __global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* 
       for (int qq = 0; qq < MAXC; ++qq) {
         const int cc = lane + 32 * qq;
         if (cc < C) {
-          Chunk<T, EPC> x[8];
+          Chunk<T, EPC> x[kPieceGroup];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < kPieceGroup; ++q)
             if (j0 + q < n) x[q] = ld_chunk<T, EPC>(srcb + (size_t)ri[q] * d + cc * EPC);
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < kPieceGroup; ++q)
             if (j0 + q < n) {
 #pragma unroll
               for (int e = 0; e < EPC; ++e)
@@ -1793,9 +1815,9 @@ __global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* 
       __threadfence();
       __syncwarp();
       uint32_t last = 0;
-      if (lane == 0) last = atomicAdd(rowdone + pd.x, 1u) == np - 1 ? 1u : 0u;
+      if (lane == 0) last = atomicAdd(A.rowdone + pd.x, 1u) == np - 1 ? 1u : 0u;
       last = __shfl_sync(0xffffffffu, last, 0);
-      if (!last) continue;
+      if (!last) return;
       __threadfence();
 #pragma unroll
       for (int qq = 0; qq < MAXC; ++qq) {
@@ -1810,7 +1832,7 @@ __global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* 
           }
         }
       }
-      if (lane == 0) rowdone[pd.x] = 0;
+
     }
     const int64_t row = side_out ? (int64_t)sg.key - A.V : (int64_t)sg.key;
     T* P = (T*)(side_out ? A.out : A.in);
@@ -1838,6 +1860,16 @@ __global__ void __launch_bounds__(256) heavy_piece(OwnerArgs A, const uint32_t* 
       A.cnt[sg.key] = 0;
     }
   }
+}
+
+// Heavy pieces as their own kernel: a small footprint (WV_PIECE_GRID CTAs of
+// WV_PIECE_THREADS) so it runs concurrently with the light-row owner.
+template <typename T, int EPC, int MAXC>
+__global__ void __launch_bounds__(WV_PIECE_THREADS) heavy_piece_kernel(OwnerArgs A) {
+  const uint32_t np_total = *(volatile const uint32_t*)(A.gctr + GC_PIECES);
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t pc = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); pc < np_total; pc += warps)
+    heavy_piece_work<T, EPC, MAXC>(A, pc);
 }
 
 // Phase 3c (split mode): RowAdam over every touched row, thread per 16-byte
@@ -2300,7 +2332,7 @@ struct LaunchOwner {
       if (dev >= 0 && dev < 16) {
         if (resident[dev] == 0) {
           int nb = 0;
-          WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_owner_flat_kernel<T, EPC>, 256, 0));
+          WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_owner_flat_kernel<T, EPC, MAXC>, 256, 0));
           resident[dev] = nb > 0 ? nb : 1;
         }
         WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2308,7 +2340,7 @@ struct LaunchOwner {
       int per = dev >= 0 && dev < 16 ? resident[dev] : 4;
       if (WV_OWNER_PER_SM > 0 && per > WV_OWNER_PER_SM) per = WV_OWNER_PER_SM;
       const unsigned g = (unsigned)(sms * per);
-      sgns_owner_flat_kernel<T, EPC><<<g, 256, 0, st>>>(a);
+      sgns_owner_flat_kernel<T, EPC, MAXC><<<g, 256, 0, st>>>(a);
       WV_LAUNCH_CHECK();
       return 0;
     }
@@ -2644,6 +2676,10 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
   oa.kmag = k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)k + 1ull) : 0xFFFFFFFFu;
   oa.cmag = 0;
   oa.ents = flat_owner(c) ? x.ents : nullptr;
+  oa.pieces = x.pieces;
+  oa.partial = x.partial;
+  oa.rowdone = x.rowdone;
+  oa.gctr = x.gctr;
   oa.segs = x.segs;
   oa.heavy = x.heavy;
   oa.seg_count = x.gctr + GC_LIGHT;
@@ -2706,12 +2742,10 @@ static int enqueue_gather(const BatchCtx& c, int h, cudaStream_t st) {
   return dispatch_rows<LaunchPair>(m->precision, c.d, pa, (const void*)m->input, (const void*)m->output, pgrid, st);
 }
 
-// owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
-// then (split mode) the Adam pass and (dense mode) the dense Adam sweep
 template <typename T, int EPC, int MAXC>
 struct LaunchPieces {
-  static int run(const OwnerArgs& a, const BatchHalf& x, cudaStream_t st) {
-    heavy_piece<T, EPC, MAXC><<<148 * 2, 256, 0, st>>>(a, x.gctr, x.pieces, (T*)x.partial, x.rowdone);
+  static int run(const OwnerArgs& a, cudaStream_t st) {
+    heavy_piece_kernel<T, EPC, MAXC><<<WV_PIECE_GRID, WV_PIECE_THREADS, 0, st>>>(a);
     WV_LAUNCH_CHECK();
     return 0;
   }
@@ -2725,10 +2759,11 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
   const int d = c.d;
   const OwnerArgs oa = owner_args(c, h);
   if (flat_owner(c)) {
-    // heavy pieces (few warps, short) first on the side stream, then the flat light-row owner
+    if (WV_OWNER_FUSED_HEAVY) return dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
+    // heavy pieces on the side stream (small footprint), concurrent with the light rows
     WV_CUDA(cudaEventRecord(ss->fork_h, st));
     WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
-    int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, c.bw.half[h], ss->h);
+    int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, ss->h);
     if (rc) return rc;
     rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
     if (rc) return rc;
