@@ -346,9 +346,9 @@ def run_ours(args, rank, world, local):
     def one_step(step, timed, profile=False):
         rb, re_ = block_range(step)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        # keep the device busy (~50 us) while the host prepares the walk launch,
+        # keep the device busy (~0.5 ms) while the host prepares the walk launch,
         # so e0 -> e1 brackets the walk kernel and not host-side launch overhead
-        torch.cuda._sleep(100_000)
+        torch.cuda._sleep(1_000_000)
         e0.record(stream)
         corpus, lengths, width = wmod.random_walks_fixed(g, ents, DEPTH, WALKS, SEED, "pcg64",
                                                          work_begin=rb * WALKS, work_count=(re_ - rb) * WALKS)

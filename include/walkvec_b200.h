@@ -39,6 +39,8 @@ extern "C" {
 #define WV_FP64 1
 
 /* SGNS pair source */
+#define WV_MODEL_SKIPGRAM 0
+#define WV_MODEL_CBOW 1
 #define WV_PAIRS_NATIVE 0   /* device Feistel permutation + length-class decode + Philox negatives */
 #define WV_PAIRS_EXPLICIT 1 /* caller-supplied pair table, epoch permutation, negatives (replay) */
 
@@ -171,9 +173,9 @@ typedef struct WvSgnsModel {
 
 typedef struct WvSgnsBatch {
   int mode; /* WV_PAIRS_NATIVE / WV_PAIRS_EXPLICIT */
-  int negatives;
+  int negatives; /* per item: negative_samples (skip-gram) or window_size (CBOW, w2v.py:481-484) */
   int window;
-  int pad;
+  int model; /* WV_MODEL_SKIPGRAM / WV_MODEL_CBOW (TrainConfig.model) */
   int64_t batch_rows;
   int64_t n_pairs;
   uint64_t seed;
@@ -195,6 +197,9 @@ typedef struct WvSgnsBatch {
    * (start, decode end, gather end, join, owner end, sort start, sort end) */
   void* timer;
   int64_t timer_base;
+  /* CBOW: instance table [n_pairs, 2*window + 1] from wv_cbow_instances
+   * (context columns, -1 padded, then the target); both pair modes index it */
+  const int32_t* instances;
 } WvSgnsBatch;
 
 int wv_sgns_init(int64_t vocab_size, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
@@ -213,8 +218,9 @@ int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, ui
                   int64_t* n_candidates, void* ws, int64_t ws_bytes, void* stream);
 /* reset the batch cursor to permuted position `start` (a worker's span start) */
 int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, void* stream);
+/* cbow_window = 0 for skip-gram, the CBOW window_size otherwise (2W context rows per item) */
 int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
-                                      int precision);
+                                      int precision, int cbow_window);
 /* copy the corpus side of `batch` (pair source, negatives) into the workspace;
  * needed before replaying a CUDA graph of wv_sgns_batch calls on a new corpus
  * (uncaptured wv_sgns_batch calls bind by themselves) */
@@ -222,8 +228,16 @@ int wv_sgns_bind(const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t v
                  int precision, void* stream);
 /* zero the workspace's persistent per-row counters: once after allocating it */
 int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size, int negatives,
-                           int64_t batch, int precision, void* stream);
+                           int64_t batch, int precision, int cbow_window, void* stream);
 int wv_sgns_batch(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, void* stream);
+/* CBOW instances (w2v.generate_cbow_instances, w2v.py:194-222): one row per
+ * token of every walk of length >= 2, in corpus order: 2*window context
+ * columns (column 2(s-1) = token s to the left, 2(s-1)+1 = s to the right,
+ * -1 when outside the walk) then the target.  Pass instances = NULL to get
+ * the count only (*n_instances, device int64). */
+int64_t wv_cbow_instances_workspace_bytes(int64_t n_walks);
+int wv_cbow_instances(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int window, int32_t* instances,
+                      int64_t* n_instances, void* ws, int64_t ws_bytes, void* stream);
 /* `count` consecutive batches, software-pipelined over the workspace's two
  * halves (decode + grouping of batch i+1 on a side stream while batch i is
  * gathered and applied); equal to `count` wv_sgns_batch calls; capturable as

@@ -3,8 +3,9 @@
 Restates /root/reference/pkg/src/walkvec/w2v.py in float64 numpy:
 init (:123-131), min_count filter + shift-major pairs (:146-191), negatives
 (:225-239, 500-504), SGNS loss/gradients (:247-299), coalescing (:407-416),
-RowAdam (:364-404), batch sizing (:437-497), _train_single (:547-576) and
-the reproducible multi-worker contract (:579-746).  Implementation choices
+RowAdam (:364-404), batch sizing (:437-497), _train_single (:547-576),
+the reproducible multi-worker contract (:579-746) and CBOW (instances
+:194-222, gradients :302-361, window_size negatives per instance :481-484).  Implementation choices
 differ from the reference on purpose (matmul dots, sort + reduceat
 coalescing) so agreement is evidence, not a copy.
 """
@@ -77,6 +78,59 @@ def sgns_step(inp, out, c, x, negs):
     return loss / B, c, gu, np.concatenate(orow), np.vstack(og)
 
 
+def cbow_instances(tokens, offsets, window: int):
+    """(ctx [N, 2W] -1 padded, lengths, targets): one instance per token of every
+    walk of length >= 2; column 2(s-1) is the token s to the left, 2(s-1)+1 to the right."""
+    rows, tg = [], []
+    for w in range(len(offsets) - 1):
+        t = tokens[offsets[w]:offsets[w + 1]]
+        L = len(t)
+        if L < 2:
+            continue
+        for i in range(L):
+            r = [-1] * (2 * window)
+            for s_ in range(1, window + 1):
+                if i - s_ >= 0:
+                    r[2 * (s_ - 1)] = t[i - s_]
+                if i + s_ < L:
+                    r[2 * (s_ - 1) + 1] = t[i + s_]
+            rows.append(r)
+            tg.append(t[i])
+    if not rows:
+        raise ValueError("empty training set")
+    ctx = np.array(rows, dtype=np.int64).reshape(-1, 2 * window)
+    return ctx, (ctx >= 0).sum(axis=1).astype(np.int64), np.array(tg, dtype=np.int64)
+
+
+def cbow_step(inp, out, ctx, lengths, targets, negs):
+    """loss + (rows, grads): context mean c, positive/negative logits against
+    output rows, grad_c / len spread over the window (w2v.py:302-361)."""
+    B, d = len(targets), inp.shape[1]
+    mask = ctx >= 0
+    c = np.zeros((B, d))
+    for col in range(ctx.shape[1]):  # masked columns add nothing
+        m = mask[:, col]
+        c[m] += inp[ctx[m, col]]
+    c /= lengths[:, None]
+    t = out[targets]
+    pos = np.matmul(c[:, None, :], t[:, :, None])[:, 0, 0]
+    loss = np.logaddexp(0.0, -pos).sum()
+    gpos = (1.0 / (1.0 + np.exp(-pos)) - 1.0) / B
+    gc = gpos[:, None] * t
+    orow, og = [targets], [gpos[:, None] * c]
+    if negs.size:
+        n = out[negs]
+        neg = np.matmul(n, c[:, :, None])[:, :, 0]
+        loss += np.logaddexp(0.0, neg).sum()
+        gneg = (1.0 / (1.0 + np.exp(-neg))) / B
+        gc = gc + (gneg[:, :, None] * n).sum(axis=1)
+        orow.append(negs.ravel())
+        og.append((gneg[:, :, None] * c[:, None, :]).reshape(-1, d))
+    per = gc / lengths[:, None]
+    b_of, col_of = np.nonzero(mask)  # row-major: the reference's contexts[mask] order
+    return loss / B, ctx[b_of, col_of], per[b_of], np.concatenate(orow), np.vstack(og)
+
+
 def coalesce(rows, grads):
     order = np.argsort(rows, kind="stable")
     r, g = rows[order], grads[order]
@@ -108,8 +162,10 @@ class RowAdam:
 
 
 def train(tokens, offsets, V, d, window, k, lr, min_count, epochs, seed, batch=None, budget=1 << 30,
-          sparse=True, max_batches=None):
-    """Single-worker SGNS (w2v.py:507-576) -> dict(inp, out, losses, touched_in, touched_out, keep)."""
+          sparse=True, max_batches=None, model="skipgram"):
+    """Single-worker SGNS or CBOW (w2v.py:507-576) -> dict(inp, out, losses, touched_in, touched_out, keep).
+
+    CBOW draws ``window`` negatives per instance (``k`` is ignored, w2v.py:481-484)."""
     tokens = np.asarray(tokens, dtype=np.int64)
     offsets = np.asarray(offsets, dtype=np.int64)
     freq = frequencies(tokens, V)
@@ -117,23 +173,38 @@ def train(tokens, offsets, V, d, window, k, lr, min_count, epochs, seed, batch=N
     ft, fo = filtered(tokens, offsets, keep)
     if len(ft) == 0:
         raise ValueError("empty training set")
-    pr = pairs(ft, fo, window)
+    cbow = model == "cbow"
+    if cbow:
+        ctx, lens, tg = cbow_instances(ft, fo, window)
+        k = window
+        n_items = len(tg)
+        per = (2 * window + 1 + window) * d * 8 + 16  # estimate_per_sample_bytes (w2v.py:437-448)
+        B = batch if batch is not None else max(1, min(budget // (4 * per), -(-n_items // 20)))
+        while B > 1 and B * per > 0.9 * budget:
+            B //= 2
+        pr = None
+    else:
+        pr = pairs(ft, fo, window)
+        n_items = len(pr)
+        B = batch_size(len(pr), d, k, budget, batch)
     cand = np.flatnonzero(keep)
     inp, out = init(V, d, seed)
-    B = batch_size(len(pr), d, k, budget, batch)
     sh = np.random.default_rng(np.random.SeedSequence([int(seed), 1, 1]))
     ng = np.random.default_rng(np.random.SeedSequence([int(seed), 1, 2, 0]))
     oi, oo = RowAdam(inp.shape, lr, sparse), RowAdam(out.shape, lr, sparse)
     ti, to = np.zeros(V, bool), np.zeros(V, bool)
     losses, nb = [], 0
     for epoch in range(epochs):
-        order = sh.permutation(len(pr))
+        order = sh.permutation(n_items)
         tot, cnt = 0.0, 0
-        for lo in range(0, len(pr), B):
+        for lo in range(0, n_items, B):
             idx = order[lo:lo + B]
             negs = cand[ng.integers(0, len(cand), size=len(idx) * k)].reshape(len(idx), k) if k else \
                 np.empty((len(idx), 0), dtype=np.int64)
-            loss, ir, ig, orr, og = sgns_step(inp, out, pr[idx, 0], pr[idx, 1], negs)
+            if cbow:
+                loss, ir, ig, orr, og = cbow_step(inp, out, ctx[idx], lens[idx], tg[idx], negs)
+            else:
+                loss, ir, ig, orr, og = sgns_step(inp, out, pr[idx, 0], pr[idx, 1], negs)
             if not np.isfinite(loss):
                 raise FloatingPointError(f"divergence at epoch {epoch}, batch {lo // B}")
             ur, ug = coalesce(ir, ig)

@@ -25,6 +25,7 @@ from .w2v import (
     TrainConfig,
     TrainingDiverged,
     estimate_per_sample_bytes,
+    generate_cbow_instances,
     generate_pairs,
     init_embeddings,
     resolve_memory_budget,
@@ -55,7 +56,7 @@ __all__ = [
     "BackendUnavailable", "EmbeddingModel", "EmbeddingTable", "Graph", "PathTable", "PipelineConfig",
     "PipelineError", "SkipGramSession", "TrainConfig", "TrainingDiverged", "Vocabulary", "Walk", "WalkCorpus",
     "bfs_walks", "build_graph", "build_vocabulary", "encode_integer_triples", "estimate_per_sample_bytes",
-    "extract_walks", "fit_transform", "generate_pairs", "init_embeddings", "install", "project_corpus",
+    "extract_walks", "fit_transform", "generate_cbow_instances", "generate_pairs", "init_embeddings", "install", "project_corpus",
     "project_entity", "project_property", "random_walks", "resolve_memory_budget", "suggest_batch_size",
     "train", "uninstall",
 ]

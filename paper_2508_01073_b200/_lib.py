@@ -25,6 +25,7 @@ FP32 = 0
 FP64 = 1
 PAIRS_NATIVE = 0
 PAIRS_EXPLICIT = 1
+MODEL_SKIPGRAM, MODEL_CBOW = 0, 1
 PHASE_PAIRS, PHASE_GROUP, PHASE_UPDATE, PHASE_ALL = 1, 2, 4, 7
 ABI_VERSION = 1
 
@@ -85,7 +86,7 @@ class WvSgnsBatch(C.Structure):
         ("mode", C.c_int),
         ("negatives", C.c_int),
         ("window", C.c_int),
-        ("pad", C.c_int),
+        ("model", C.c_int),
         ("batch_rows", C.c_int64),
         ("n_pairs", C.c_int64),
         ("seed", C.c_uint64),
@@ -103,6 +104,7 @@ class WvSgnsBatch(C.Structure):
         ("negative_table", C.c_void_p),
         ("timer", C.c_void_p),
         ("timer_base", C.c_int64),
+        ("instances", C.c_void_p),
     ]
 
 
@@ -148,8 +150,10 @@ SIGNATURES = {
     "wv_candidates_workspace_bytes": (I64, [I64]),
     "wv_candidates": (I32, [P, I64, I64, P, P, P, P, I64, P]),
     "wv_sgns_epoch_begin": (I32, [P, I64, I64, P]),
-    "wv_sgns_batch_workspace_bytes": (I64, [I64, I32, I32, I64, I32]),
-    "wv_sgns_workspace_init": (I32, [P, I64, I64, I32, I32, I64, I32, P]),
+    "wv_sgns_batch_workspace_bytes": (I64, [I64, I32, I32, I64, I32, I32]),
+    "wv_sgns_workspace_init": (I32, [P, I64, I64, I32, I32, I64, I32, I32, P]),
+    "wv_cbow_instances_workspace_bytes": (I64, [I64]),
+    "wv_cbow_instances": (I32, [P, P, I64, I32, P, P, P, I64, P]),
     "wv_sgns_bind": (I32, [P, P, I64, I64, I32, I32, P]),
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),

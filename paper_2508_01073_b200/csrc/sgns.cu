@@ -231,7 +231,7 @@ struct CorpusDesc {
   int mode;  // WV_PAIRS_NATIVE or WV_PAIRS_EXPLICIT
   int window;
   int n_classes;
-  int pad;
+  int model;  // WV_MODEL_SKIPGRAM or WV_MODEL_CBOW
   int64_t N;  // pairs per epoch
   uint64_t seed;
   // native corpus index
@@ -247,12 +247,16 @@ struct CorpusDesc {
   const int32_t* pairs;      // [N,2]
   const int64_t* perm;       // [N] epoch permutation
   const int32_t* negatives;  // [N,k] per permuted position
+  // CBOW instance table [N, 2W + 1] (context columns then the target)
+  const int32_t* inst;
 };
 
 struct PairArgs {
   int64_t V;
   int d;
   int k;
+  int R;   // rows per item: 2 + k (skip-gram) or 2W + 1 + k (CBOW)
+  int cw;  // CBOW window W (0: skip-gram)
   int64_t B;  // rows in this batch
   const CorpusDesc* desc;
   // outputs
@@ -292,12 +296,25 @@ __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
 // (Feistel position -> length class -> walk -> window slot: a chain of
 // dependent L2 reads) and writes centre and context; items j >= 2 draw one
 // negative each.  Thread-per-item spreads the latency chains over all SMs.
+// one negative: Philox4x32 counter (position, epoch, j/2), two draws per call,
+// uniform over the candidates; or the replayed numpy stream
+__device__ __forceinline__ int32_t draw_negative(const CorpusDesc& D, int64_t pos, uint64_t epoch, int j, int k) {
+  if (D.mode == WV_PAIRS_NATIVE) {
+    uint32_t rnd[4] = {(uint32_t)pos, (uint32_t)((uint64_t)pos >> 32), (uint32_t)epoch, (uint32_t)(j >> 1)};
+    philox4x32_10(rnd, (uint32_t)D.seed ^ 0xA5A5F00Du, (uint32_t)(D.seed >> 32) ^ 0x3C6EF372u);
+    const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
+    const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)D.n_candidates);
+    return D.candidates ? D.candidates[ci] : (int32_t)ci;
+  }
+  return D.negatives[pos * k + j];
+}
+
 __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
   __shared__ CorpusDesc D;
   if (threadIdx.x == 0) D = *A.desc;
   __syncthreads();
   const int k = A.k;
-  const int R = 2 + k;
+  const int R = A.R;
   const int64_t B = A.B;
   const int64_t items = B * R;
   const int64_t lo = A.state->lo;
@@ -310,6 +327,22 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
     const int jj = (int)(it - b * R);
     const int64_t pos = lo + b;
     int32_t* row = A.idx + b * R;
+    if (A.cw > 0) {
+      // CBOW: items 0..2W-1 the context rows (input side, -1 outside the walk),
+      // 2W the target and 2W+1.. the negatives (output side)
+      const int ctxw = 2 * A.cw;
+      if (jj <= ctxw) {
+        const int64_t q = D.mode == WV_PAIRS_NATIVE ? (int64_t)feistel_perm(fs, (uint64_t)pos, D.N) : D.perm[pos];
+        const int32_t t = D.inst[q * (ctxw + 1) + jj];
+        row[jj] = t;
+        if (t >= 0) group_claim(A, (uint32_t)t + (jj == ctxw ? (uint32_t)A.V : 0u));
+      } else {
+        const int32_t neg = draw_negative(D, pos, epoch, jj - ctxw - 1, k);
+        row[jj] = neg;
+        group_claim(A, (uint32_t)(neg + A.V));
+      }
+      continue;
+    }
     if (jj == 0) {
       int32_t center, context;
       if (D.mode == WV_PAIRS_NATIVE) {
@@ -340,18 +373,7 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       group_claim(A, (uint32_t)center);
       group_claim(A, (uint32_t)(context + A.V));
     } else if (jj >= 2) {
-      const int j = jj - 2;
-      int32_t neg;
-      if (D.mode == WV_PAIRS_NATIVE) {
-        // Philox4x32 counter (position, epoch, j/2): two draws per call
-        uint32_t rnd[4] = {(uint32_t)pos, (uint32_t)((uint64_t)pos >> 32), (uint32_t)epoch, (uint32_t)(j >> 1)};
-        philox4x32_10(rnd, (uint32_t)D.seed ^ 0xA5A5F00Du, (uint32_t)(D.seed >> 32) ^ 0x3C6EF372u);
-        const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
-        const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)D.n_candidates);
-        neg = D.candidates ? D.candidates[ci] : (int32_t)ci;
-      } else {
-        neg = D.negatives[pos * k + j];
-      }
+      const int32_t neg = draw_negative(D, pos, epoch, jj - 2, k);
       row[jj] = neg;
       group_claim(A, (uint32_t)(neg + A.V));
     }
@@ -437,13 +459,18 @@ constexpr int kBulkThreads = kBulkWarps * 32;
 // and the next pair's rows land while this pair computes; no row data is held
 // in registers across the wait, which keeps occupancy up.  Lanes 0..k each
 // evaluate one loss term (the reference's float64 logaddexp, w2v.py:262-273).
-template <typename T, int EPC, int MAXC>
-__global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs A, const T* __restrict__ in,
-                                                                         const T* __restrict__ out) {
+// CB = CBOW (w2v.py:302-361): the item is an instance whose up-to-2W context
+// rows are averaged into u = c (the masked mean), its target row takes the
+// positive logit, and the input-side gradient is grad_c / len.
+template <typename T, int EPC, int MAXC, bool CB, int NW>
+__global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, const T* __restrict__ in,
+                                                                    const T* __restrict__ out) {
+  constexpr int kBulkWarps = NW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = A.d, k = A.k;
-  const int R = 2 + k;
+  const int R = CB ? A.R : 2 + k;
+  const int ctxw = CB ? 2 * A.cw : 1;  // input-side rows per item; the positive output row follows them
   const int C = d / EPC;
   const int64_t B = A.B;
   const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
@@ -464,12 +491,13 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
   int64_t b = blockIdx.x * (int64_t)kBulkWarps + warp;
   auto issue = [&](int64_t pb, int stage) {
     T* dst = ring + (size_t)stage * R * d;
-    int32_t r = 0;
+    int32_t r = -1;
     if (lane < R) r = __ldg(A.idx + pb * R + lane);
-    if (lane == 0) mbar_arrive_expect_tx(mybar + stage, row_bytes * (uint32_t)R);
+    const uint32_t valid = __ballot_sync(0xffffffffu, lane < R && r >= 0);  // CBOW: masked context columns
+    if (lane == 0) mbar_arrive_expect_tx(mybar + stage, row_bytes * (uint32_t)__popc(valid));
     __syncwarp();
-    if (lane < R) {
-      const T* src = (lane == 0 ? in : out) + (int64_t)r * d;
+    if ((valid >> lane) & 1u) {
+      const T* src = (lane < ctxw ? in : out) + (int64_t)r * d;
       bulk_row_g2s(dst + (size_t)lane * d, src, row_bytes, mybar + stage);
     }
   };
@@ -491,13 +519,38 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
     phase ^= 1u << stage;
     const T* rows = ring + (size_t)stage * R * d;
     Chunk<T, EPC> u[MAXC];
+    T len_t = 1;
+    if constexpr (CB) {
+      // c = masked mean of the context rows, summed in column order (w2v.py:308)
+      const int32_t t = lane < ctxw ? __ldg(A.idx + b * R + lane) : -1;
+      const uint32_t cm = __ballot_sync(0xffffffffu, t >= 0);
+      const T len = (T)__popc(cm);
+      len_t = len;
 #pragma unroll
-    for (int q = 0; q < MAXC; ++q) {
-      const int c = lane + 32 * q;
-      if (c < C) u[q] = *reinterpret_cast<const Chunk<T, EPC>*>(rows + c * EPC);
+      for (int q = 0; q < MAXC; ++q) {
+        const int c = lane + 32 * q;
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) u[q].v[e] = 0;
+        if (c < C) {
+          for (int j = 0; j < ctxw; ++j)
+            if ((cm >> j) & 1u) {
+              const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)j * d + c * EPC);
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) u[q].v[e] = add_rn(u[q].v[e], x.v[e]);
+            }
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) u[q].v[e] = div_rn(u[q].v[e], len);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int c = lane + 32 * q;
+        if (c < C) u[q] = *reinterpret_cast<const Chunk<T, EPC>*>(rows + c * EPC);
+      }
     }
-    // dot j = <u, row 1+j> (j = 0: context, j >= 1: negative j-1), eight at a
-    // time through one transposed butterfly; lane j ends up holding dot j
+    // dot j = <u, row ctxw+j> (j = 0: context / target, j >= 1: negative j-1),
+    // eight at a time through one transposed butterfly; lane j ends up holding dot j
     T mydot = 0;
     for (int j0 = 0; j0 <= k; j0 += 8) {
       T part[8];
@@ -505,7 +558,7 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
       for (int t = 0; t < 8; ++t) {
         part[t] = 0;
         if (j0 + t <= k) {
-          const T* rj = rows + (size_t)(1 + j0 + t) * d;
+          const T* rj = rows + (size_t)(ctxw + j0 + t) * d;
 #pragma unroll
           for (int q = 0; q < MAXC; ++q) {
             const int c = lane + 32 * q;
@@ -539,16 +592,22 @@ __global__ void __launch_bounds__(kBulkThreads) sgns_gather_bulk_kernel(PairArgs
       for (int j = 1; j <= k; ++j) {
         const T gneg = __shfl_sync(0xffffffffu, mycoef, j);
         if (c < C) {
-          const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)(1 + j) * d + c * EPC);
+          const Chunk<T, EPC> x =
+              *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)(ctxw + j) * d + c * EPC);
 #pragma unroll
           for (int e = 0; e < EPC; ++e) acc.v[e] = mad_t(gneg, x.v[e], acc.v[e]);
         }
       }
       if (c < C) {
-        const Chunk<T, EPC> v = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)d + c * EPC);
+        const Chunk<T, EPC> v = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)ctxw * d + c * EPC);
         Chunk<T, EPC> gg;
 #pragma unroll
         for (int e = 0; e < EPC; ++e) gg.v[e] = mad_t(gpos, v.v[e], acc.v[e]);
+        if constexpr (CB) {
+          // per-context-token share grad_c / len (w2v.py:356)
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) gg.v[e] = div_rn(gg.v[e], len_t);
+        }
         st_chunk<T, EPC>(G + b * d + c * EPC, gg);
         st_chunk<T, EPC>(U + b * d + c * EPC, u[q]);
       }
@@ -806,38 +865,69 @@ __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __re
 }
 
 // every item appends its slot to its row's list
-__global__ void group_place(const int32_t* __restrict__ idx, int64_t B, int k, int64_t V, uint32_t* __restrict__ cnt,
-                            uint32_t* __restrict__ list) {
-  const int64_t items = B * (2 + k);
+// Slots (the order np.add.at applies contributions, w2v.py:407-416):
+//   skip-gram: centre b -> b; context b -> B + b; negative j -> 2B + bk + j
+//   CBOW     : context column c of instance b -> b*2W + c (input side);
+//              target b -> b; negative j -> B + bk + j (output side)
+// so an output slot minus out_base (B for skip-gram, 0 for CBOW) is < B for
+// the positive row and B + bk + j for negative j in both models.
+__global__ void group_place(const int32_t* __restrict__ idx, int64_t B, int k, int R, int cw, int64_t V,
+                            uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
+  const int64_t items = B * R;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < items; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = i / (2 + k);
-    const int j = (int)(i - b * (2 + k));
-    const uint32_t key = (uint32_t)idx[i] + (j == 0 ? 0u : (uint32_t)V);
-    const uint32_t slot = (uint32_t)(j == 0 ? b : (j == 1 ? B + b : 2 * B + b * k + (j - 2)));
+    const int64_t b = i / R;
+    const int j = (int)(i - b * R);
+    const int32_t t = idx[i];
+    uint32_t key, slot;
+    if (cw == 0) {
+      key = (uint32_t)t + (j == 0 ? 0u : (uint32_t)V);
+      slot = (uint32_t)(j == 0 ? b : (j == 1 ? B + b : 2 * B + b * k + (j - 2)));
+    } else {
+      if (t < 0) continue;  // context column outside the walk
+      const int ctxw = 2 * cw;
+      key = (uint32_t)t + (j < ctxw ? 0u : (uint32_t)V);
+      slot = (uint32_t)(j < ctxw ? b * ctxw + j : (j == ctxw ? b : B + b * k + (j - ctxw - 1)));
+    }
     list[atomicAdd(cnt + key, 1u)] = slot;
   }
 }
 
+// Slot-to-source mapping parameters (skip-gram / CBOW).
+struct SlotMap {
+  uint32_t out_base;  // B (skip-gram) or 0 (CBOW)
+  uint32_t in_div;    // input slot -> G row: slot / in_div (1 or 2W)
+  uint32_t in_mag;    // ~2^32 / in_div
+  uint32_t kmag;      // ~2^32 / k
+};
+
+__device__ __forceinline__ uint32_t div_mag(uint32_t t, uint32_t dv, uint32_t mag, int32_t& rem) {
+  uint32_t q = __umulhi(t, mag);
+  int32_t r = (int32_t)(t - q * dv);
+  if (r < 0) {
+    --q;
+    r += (int32_t)dv;
+  } else if (r >= (int32_t)dv) {
+    ++q;
+    r -= (int32_t)dv;
+  }
+  rem = r;
+  return q;
+}
+
+static inline uint32_t host_mag(uint32_t dv) { return dv > 1 ? (uint32_t)(0xFFFFFFFFull / dv + 1ull) : 0xFFFFFFFFu; }
+
 // Contribution slot -> (source U/G row, coefficient index); ci = 0xffffffff
 // marks an input-side contribution (G row, coefficient 1).
-__device__ __forceinline__ uint2 slot_entry(uint32_t v, bool side_out, int64_t B, int k, uint32_t kmag) {
-  if (!side_out) return make_uint2(v, 0xffffffffu);
-  const uint32_t sv = v - (uint32_t)B;
+__device__ __forceinline__ uint2 slot_entry(uint32_t v, bool side_out, int64_t B, int k, const SlotMap& sm) {
+  int32_t r;
+  if (!side_out) return make_uint2(sm.in_div == 1 ? v : div_mag(v, sm.in_div, sm.in_mag, r), 0xffffffffu);
+  const uint32_t sv = v - sm.out_base;
   uint32_t pp, j;
   if (sv < (uint32_t)B) {
     pp = sv;
     j = 0;
   } else {
-    const uint32_t t = sv - (uint32_t)B;
-    pp = __umulhi(t, kmag);
-    int32_t r = (int32_t)(t - pp * (uint32_t)k);
-    if (r < 0) {
-      --pp;
-      r += k;
-    } else if (r >= k) {
-      ++pp;
-      r -= k;
-    }
+    pp = div_mag(sv - (uint32_t)B, (uint32_t)k, sm.kmag, r);
     j = 1 + (uint32_t)r;
   }
   return make_uint2(pp, pp * (uint32_t)(k + 1) + j);
@@ -851,7 +941,7 @@ __device__ __forceinline__ uint2 slot_entry(uint32_t v, bool side_out, int64_t B
 // contribution (G row, coefficient 1).
 __global__ void group_order(const Segment* __restrict__ segs, const uint32_t* __restrict__ gctr,
                             const uint32_t* __restrict__ list, uint2* __restrict__ ents, int64_t V, int64_t B, int k,
-                            uint32_t kmag) {
+                            SlotMap sm) {
   const uint32_t nl = *(volatile const uint32_t*)(gctr + GC_LIGHT);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
     const Segment sg = segs[i];
@@ -872,7 +962,7 @@ __global__ void group_order(const Segment* __restrict__ segs, const uint32_t* __
 #pragma unroll
     for (int q = 0; q < kLightMax; ++q) {
       if (q >= (int)sg.len) break;
-      ents[sg.start + q] = slot_entry(sl[q], side_out, B, k, kmag);
+      ents[sg.start + q] = slot_entry(sl[q], side_out, B, k, sm);
     }
   }
 }
@@ -887,7 +977,7 @@ struct OwnerArgs {
   uint32_t* list_tmp;    // scratch for the heavy rows' slot sort
   uint32_t* cnt;         // reset to 0 per row once consumed
   int slot_bits;         // bits of the largest slot (2B + Bk - 1)
-  uint32_t kmag;         // ~2^32 / k for the slot -> (pair, negative) split
+  SlotMap sm;            // slot -> (source row, coefficient) mapping of the model
   uint32_t cmag;         // ~2^32 / (d / EPC) for the flat owner's (row, chunk) split
   const uint2* ents;     // slot-ordered (source row, coefficient index), from group_order / heavy_order
   const uint2* pieces;   // heavy-row pieces (row, piece index) from heavy_order
@@ -976,33 +1066,11 @@ __device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, const AdamBC<T>& b
 // take the pair's centre gradient row G[b] (coefficient 1); output-matrix rows
 // take coef * U[b] (the context's gpos or negative j's gneg).
 template <typename T>
-__device__ __forceinline__ uint32_t contribution(uint32_t v, bool side_out, int64_t B, int k, uint32_t kmag,
+__device__ __forceinline__ uint32_t contribution(uint32_t v, bool side_out, int64_t B, int k, const SlotMap& sm,
                                                  const T* coef, T& c) {
-  if (!side_out) {
-    c = 1;
-    return v;  // G row
-  }
-  const uint32_t s = v - (uint32_t)B;
-  uint32_t pp, j;
-  if (s < (uint32_t)B) {
-    pp = s;
-    j = 0;
-  } else {
-    // t / k by multiply-high with a one-step correction (kmag ~ 2^32 / k)
-    const uint32_t t = s - (uint32_t)B;
-    pp = __umulhi(t, kmag);
-    int32_t r = (int32_t)(t - pp * (uint32_t)k);
-    if (r < 0) {
-      --pp;
-      r += k;
-    } else if (r >= k) {
-      ++pp;
-      r -= k;
-    }
-    j = 1 + (uint32_t)r;
-  }
-  c = __ldg(coef + (int64_t)pp * (k + 1) + j);
-  return pp;  // U row
+  const uint2 e = slot_entry(v, side_out, B, k, sm);
+  c = side_out ? __ldg(coef + e.y) : T(1);
+  return e.x;  // G row (input side) or U row (output side)
 }
 
 // Phase 3: one warp per (unique row, 32-chunk slice of the row): sum the row's
@@ -1051,7 +1119,7 @@ __global__ void __launch_bounds__(kOwnerThreads, WV_OWNER_MINB) sgns_owner_kerne
     mt.myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
     mt.my_c = 0;
     mt.my_ri = 0;
-    if (lane < (int)sg.len) mt.my_ri = contribution<T>(mt.myslot, sg.key >= (uint32_t)A.V, B, k, A.kmag, coef, mt.my_c);
+    if (lane < (int)sg.len) mt.my_ri = contribution<T>(mt.myslot, sg.key >= (uint32_t)A.V, B, k, A.sm, coef, mt.my_c);
   };
   Meta nxt;
   if (gw < slots) load_meta(gw, nxt);
@@ -1200,7 +1268,7 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
     const uint32_t myslot = lane < (int)sg.len ? A.list[sg.start + lane] : 0xffffffffu;
     mt.my_c = 0;
     mt.my_ri = 0;
-    if (lane < (int)sg.len) mt.my_ri = contribution<T>(myslot, sg.key >= (uint32_t)A.V, B, k, A.kmag, coef, mt.my_c);
+    if (lane < (int)sg.len) mt.my_ri = contribution<T>(myslot, sg.key >= (uint32_t)A.V, B, k, A.sm, coef, mt.my_c);
     int r = 0;
     for (int j = 0; j < (int)sg.len; ++j) r += __shfl_sync(0xffffffffu, myslot, j) < myslot;
     mt.myrank = lane < (int)sg.len ? r : 64;
@@ -1604,7 +1672,7 @@ __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kerne
       const uint32_t n32 = min(32u, hi - i0);
       T my_c = 0;
       uint32_t my_ri = 0;
-      if ((uint32_t)lane < n32) my_ri = contribution<T>(sorted[i0 + lane], side_out, B, k, A.kmag, coef, my_c);
+      if ((uint32_t)lane < n32) my_ri = contribution<T>(sorted[i0 + lane], side_out, B, k, A.sm, coef, my_c);
       for (uint32_t j0 = 0; j0 < n32; j0 += kHeavyGroup) {
         const int nq = (int)min((uint32_t)kHeavyGroup, n32 - j0);
         uint32_t ri[kHeavyGroup];
@@ -1735,7 +1803,7 @@ __global__ void __launch_bounds__(kHeavyThreads) heavy_order(OwnerArgs A, uint32
                               sort_hist);
     }
     for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads)
-      ents[sg.start + i] = slot_entry(sorted[i], side_out, A.B, A.k, A.kmag);
+      ents[sg.start + i] = slot_entry(sorted[i], side_out, A.B, A.k, A.sm);
     const uint32_t np = (sg.len + kPiece - 1) / kPiece;
     if (threadIdx.x == 0) {
       s_pbase = atomicAdd(gctr + GC_PIECES, np);
@@ -2025,6 +2093,32 @@ __global__ void pairs_per_walk(const int64_t* __restrict__ offsets, int64_t n_wa
   }
 }
 
+// CBOW instances (generate_cbow_instances, w2v.py:194-222): every token of a
+// walk of length >= 2 is one instance, in corpus order.
+__global__ void cbow_counts(const int64_t* __restrict__ offsets, int64_t n_walks, int64_t* __restrict__ cnt) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t L = offsets[w + 1] - offsets[w];
+    cnt[w] = L >= 2 ? L : 0;
+  }
+}
+
+__global__ void cbow_emit(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets, int64_t n_walks,
+                          int window, const int64_t* __restrict__ base, int32_t* __restrict__ inst) {
+  const int cols = 2 * window + 1;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_walks; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = offsets[w], L = offsets[w + 1] - o;
+    if (L < 2) continue;
+    for (int64_t i = 0; i < L; ++i) {
+      int32_t* row = inst + (base[w] + i) * cols;
+      for (int s = 1; s <= window; ++s) {
+        row[2 * (s - 1)] = i - s >= 0 ? tokens[o + i - s] : -1;
+        row[2 * (s - 1) + 1] = i + s < L ? tokens[o + i + s] : -1;
+      }
+      row[2 * window] = tokens[o + i];
+    }
+  }
+}
+
 __global__ void pairs_emit(const int32_t* __restrict__ tokens, const int64_t* __restrict__ offsets, int64_t n_walks,
                            int s, const int64_t* __restrict__ prefix, const int64_t* __restrict__ n_s_p,
                            int64_t block_base, int32_t* __restrict__ pairs) {
@@ -2120,50 +2214,67 @@ static int dispatch_rows(int precision, int d, Args&&... args) {
   return -1;
 }
 
-// shared memory of the bulk gather: barriers + per-warp two-stage ring of 2+k rows
-static inline size_t bulk_smem_bytes(int d, int k, size_t es) {
-  return 16 * kBulkWarps * kBulkStages + (size_t)kBulkWarps * kBulkStages * (2 + k) * d * es;
+// shared memory of the bulk gather: barriers + per-warp ring of R rows per stage
+static inline size_t bulk_smem_bytes(int nw, int d, int R, size_t es) {
+  return 16 * nw * kBulkStages + (size_t)nw * kBulkStages * R * d * es;
 }
 static constexpr size_t kBulkSmemMax = 220 * 1024;
+
+// one bulk-gather instantiation: smem attribute, persistent grid of resident CTAs
+template <typename T, int EPC, int MAXC, bool CB, int NW>
+static int launch_bulk_gather(const PairArgs& a, const void* in, const void* out, size_t smem, cudaStream_t st) {
+  auto kern = sgns_gather_bulk_kernel<T, EPC, MAXC, CB, NW>;
+  static size_t attr_set[16] = {0};
+  static int resident[16] = {0};
+  static size_t resident_smem[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  if (dev >= 0 && dev < 16) {
+    if (attr_set[dev] < smem) {
+      WV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set[dev] = smem;
+    }
+    if (resident[dev] == 0 || resident_smem[dev] != smem) {
+      int nb = 0;
+      WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NW * 32, smem));
+      resident[dev] = nb > 0 ? nb : 1;
+      resident_smem[dev] = smem;
+    }
+    WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t blocks = (a.B + NW - 1) / NW;
+  const int64_t cap = (int64_t)sms * (dev >= 0 && dev < 16 ? resident[dev] : 4);
+  const unsigned g = (unsigned)(blocks < cap ? blocks : cap);
+  kern<<<g, NW * 32, smem, st>>>(a, (const T*)in, (const T*)out);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
 
 template <typename T, int EPC, int MAXC>
 struct LaunchPair {
   // register path: negatives gathered per group, as many as fit in registers
   static constexpr int NG = MAXC <= 2 ? 5 : (MAXC <= 4 ? 2 : 1);
   static int run(const PairArgs& a, const void* in, const void* out, unsigned grid, cudaStream_t st) {
-    const size_t smem = bulk_smem_bytes(a.d, a.k, sizeof(T));
-    const bool bulk = (a.d * sizeof(T)) % 16 == 0 && EPC * sizeof(T) == 16 && smem <= kBulkSmemMax &&
-                      getenv("WV_SGNS_REG_GATHER") == nullptr;
-    if (bulk) {
-      static size_t attr_set[16] = {0};
-      int dev = 0;
-      cudaGetDevice(&dev);
-      if (dev >= 0 && dev < 16 && attr_set[dev] < smem) {
-        WV_CUDA(cudaFuncSetAttribute(sgns_gather_bulk_kernel<T, EPC, MAXC>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set[dev] = smem;
+    const bool rows16 = (a.d * sizeof(T)) % 16 == 0 && EPC * sizeof(T) == 16;
+    if (a.cw > 0) {
+      // CBOW: bulk path only, warps per CTA chosen so the ring fits in shared memory
+      WV_CHECK_ARG(rows16, "CBOW needs vector_size * element size to be a multiple of 16 bytes");
+      for (int nw : {8, 4, 2, 1}) {
+        const size_t smem = bulk_smem_bytes(nw, a.d, a.R, sizeof(T));
+        if (smem > kBulkSmemMax) continue;
+        if (nw == 8) return launch_bulk_gather<T, EPC, MAXC, true, 8>(a, in, out, smem, st);
+        if (nw == 4) return launch_bulk_gather<T, EPC, MAXC, true, 4>(a, in, out, smem, st);
+        if (nw == 2) return launch_bulk_gather<T, EPC, MAXC, true, 2>(a, in, out, smem, st);
+        return launch_bulk_gather<T, EPC, MAXC, true, 1>(a, in, out, smem, st);
       }
-      // persistent grid: exactly the resident CTAs (no partial second wave)
-      static int resident[16] = {0};
-      static size_t resident_smem[16] = {0};
-      int sms = 148;
-      if (dev >= 0 && dev < 16) {
-        if (resident[dev] == 0 || resident_smem[dev] != smem) {
-          int nb = 0;
-          WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_gather_bulk_kernel<T, EPC, MAXC>,
-                                                                 kBulkThreads, smem));
-          resident[dev] = nb > 0 ? nb : 1;
-          resident_smem[dev] = smem;
-        }
-        WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      }
-      const int64_t blocks = (a.B + kBulkWarps - 1) / kBulkWarps;
-      const int64_t cap = (int64_t)sms * (dev >= 0 && dev < 16 ? resident[dev] : 4);
-      const unsigned g = (unsigned)(blocks < cap ? blocks : cap);
-      sgns_gather_bulk_kernel<T, EPC, MAXC><<<g, kBulkThreads, smem, st>>>(a, (const T*)in, (const T*)out);
-    } else {
-      sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
+      set_error("CBOW window too large for the shared-memory ring (vector_size %d)", a.d);
+      return -1;
     }
+    const size_t smem = bulk_smem_bytes(kBulkWarps, a.d, 2 + a.k, sizeof(T));
+    if (rows16 && smem <= kBulkSmemMax && getenv("WV_SGNS_REG_GATHER") == nullptr)
+      return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps>(a, in, out, smem, st);
+    sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
     WV_LAUNCH_CHECK();
     return 0;
   }
@@ -2235,8 +2346,11 @@ struct BatchWs {
 
 static bool split_adam_requested() { return getenv("WV_SGNS_SPLIT_ADAM") != nullptr; }
 
-static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int64_t B, int64_t es, BatchWs& w) {
-  const int64_t items = B * (2 + k);
+// rows per item: 2 + k (skip-gram) or 2W + 1 + k (CBOW)
+static inline int rows_per_item(int k, int cbow_window) { return cbow_window > 0 ? 2 * cbow_window + 1 + k : 2 + k; }
+
+static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int R, int64_t B, int64_t es, BatchWs& w) {
+  const int64_t items = B * R;
   int64_t off = 0;
   auto take = [&](int64_t bytes) -> void* {
     void* p = base ? base + off : nullptr;
@@ -2274,7 +2388,7 @@ static CorpusDesc make_desc(const WvSgnsBatch* b) {
   c.mode = b->mode;
   c.window = b->window;
   c.n_classes = (int)b->n_classes;
-  c.pad = 0;
+  c.model = b->model;
   c.N = b->n_pairs;
   c.seed = b->seed;
   c.tokens = b->tokens;
@@ -2288,6 +2402,7 @@ static CorpusDesc make_desc(const WvSgnsBatch* b) {
   c.pairs = b->pairs;
   c.perm = b->perm;
   c.negatives = b->negative_table;
+  c.inst = b->instances;
   return c;
 }
 
@@ -2517,6 +2632,34 @@ int wv_generate_pairs(const int32_t* tokens, const int64_t* offsets, int64_t n_w
   return 0;
 }
 
+int64_t wv_cbow_instances_workspace_bytes(int64_t n_walks) {
+  using namespace wv;
+  return al256(n_walks * 8) * 2 + al256(scan_tiles(n_walks) * 8) + 256;
+}
+
+int wv_cbow_instances(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, int window, int32_t* instances,
+                      int64_t* n_instances, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(window >= 1, "window must be >= 1");
+  WV_CHECK_ARG(n_walks >= 1, "empty corpus");
+  WV_CHECK_ARG(ws_bytes >= wv_cbow_instances_workspace_bytes(n_walks), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int64_t* cnt = (int64_t*)w;
+  w += al256(n_walks * 8);
+  int64_t* base = (int64_t*)w;
+  w += al256(n_walks * 8);
+  int64_t* scan_ws = (int64_t*)w;
+  cbow_counts<<<grid_for(n_walks, 256), 256, 0, st>>>(offsets, n_walks, cnt);
+  WV_LAUNCH_CHECK();
+  WV_CUDA((excl_scan<int64_t, int64_t>(cnt, n_walks, base, n_instances, scan_ws, st)));
+  if (instances) {
+    cbow_emit<<<grid_for(n_walks, 128), 128, 0, st>>>(tokens, offsets, n_walks, window, base, instances);
+    WV_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
 int64_t wv_candidates_workspace_bytes(int64_t vocab_size) {
   using namespace wv;
   return al256(vocab_size) + al256(vocab_size * 8) + al256(scan_tiles(vocab_size) * 8) + 256;
@@ -2549,20 +2692,21 @@ int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, voi
 }
 
 int64_t wv_sgns_batch_workspace_bytes(int64_t vocab_size, int vector_size, int negatives, int64_t batch,
-                                      int precision) {
+                                      int precision, int cbow_window) {
   using namespace wv;
   BatchWs bw;
-  return carve_batch_ws(nullptr, vocab_size, vector_size, negatives, batch, precision == WV_FP64 ? 8 : 4, bw);
+  return carve_batch_ws(nullptr, vocab_size, vector_size, negatives, rows_per_item(negatives, cbow_window), batch,
+                        precision == WV_FP64 ? 8 : 4, bw);
 }
 
 // Zero the workspace's persistent per-row counters; required once after the
 // workspace is allocated (every batch leaves them zero again).
 int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int vector_size, int negatives,
-                           int64_t batch, int precision, void* stream) {
+                           int64_t batch, int precision, int cbow_window, void* stream) {
   using namespace wv;
   BatchWs bw;
-  const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, negatives, batch,
-                                      precision == WV_FP64 ? 8 : 4, bw);
+  const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, negatives,
+                                      rows_per_item(negatives, cbow_window), batch, precision == WV_FP64 ? 8 : 4, bw);
   WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
   for (int h = 0; h < 2; ++h) WV_CUDA(cudaMemsetAsync(bw.half[h].cnt, 0, 2 * vocab_size * 4, (cudaStream_t)stream));
   return 0;
@@ -2577,7 +2721,9 @@ int wv_sgns_bind(const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t v
   using namespace wv;
   WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
   BatchWs bw;
-  const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, batch->negatives, batch->batch_rows,
+  const int cw = batch->model == WV_MODEL_CBOW ? batch->window : 0;
+  const int64_t need = carve_batch_ws((char*)ws, vocab_size, vector_size, batch->negatives,
+                                      rows_per_item(batch->negatives, cw), batch->batch_rows,
                                       precision == WV_FP64 ? 8 : 4, bw);
   WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
   const CorpusDesc c = make_desc(batch);
@@ -2594,6 +2740,8 @@ struct BatchCtx {
   const WvSgnsModel* model;
   int64_t V, B, items, es;
   int d, k;
+  int R, cw;  // rows per item, CBOW window (0: skip-gram)
+  SlotMap sm;
   BatchWs bw;
   void* timer;
   int tb;
@@ -2608,11 +2756,20 @@ static int batch_ctx(const WvSgnsModel* model, const WvSgnsBatch* batch, void* w
   WV_CHECK_ARG(c.B >= 1, "empty batch");
   WV_CHECK_ARG(c.k >= 0 && c.k <= 30, "negative_samples must be in [0, 30]");
   WV_CHECK_ARG(2 * c.V < (int64_t)0xffffffffLL, "vocabulary too large for 32-bit row keys");
-  WV_CHECK_ARG(c.B * (2 + c.k) < (int64_t)0x7fffffffLL, "batch too large");
   WV_CHECK_ARG(batch->mode == WV_PAIRS_NATIVE || batch->mode == WV_PAIRS_EXPLICIT, "bad pair mode");
+  WV_CHECK_ARG(batch->model == WV_MODEL_SKIPGRAM || batch->model == WV_MODEL_CBOW, "bad model %d", batch->model);
+  c.cw = batch->model == WV_MODEL_CBOW ? batch->window : 0;
+  WV_CHECK_ARG(c.cw == 0 || (c.cw >= 1 && c.cw <= 15 && batch->instances != nullptr),
+               "CBOW needs window_size in [1, 15] and an instance table");
+  c.R = rows_per_item(c.k, c.cw);
+  WV_CHECK_ARG(c.B * c.R < (int64_t)0x7fffffffLL, "batch too large");
   c.es = model->precision == WV_FP64 ? 8 : 4;
-  c.items = c.B * (2 + c.k);
-  const int64_t need = carve_batch_ws((char*)ws, c.V, c.d, c.k, c.B, c.es, c.bw);
+  c.items = c.B * c.R;
+  c.sm.out_base = c.cw ? 0u : (uint32_t)c.B;
+  c.sm.in_div = c.cw ? (uint32_t)(2 * c.cw) : 1u;
+  c.sm.in_mag = host_mag(c.sm.in_div);
+  c.sm.kmag = host_mag((uint32_t)(c.k > 0 ? c.k : 1));
+  const int64_t need = carve_batch_ws((char*)ws, c.V, c.d, c.k, c.R, c.B, c.es, c.bw);
   WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
   c.timer = batch->timer;
   c.tb = (int)batch->timer_base;
@@ -2624,6 +2781,8 @@ static PairArgs pair_args(const BatchCtx& c, int h) {
   pa.V = c.V;
   pa.d = c.d;
   pa.k = c.k;
+  pa.R = c.R;
+  pa.cw = c.cw;
   pa.B = c.B;
   pa.desc = c.bw.desc;
   pa.U = c.bw.U;
@@ -2673,7 +2832,7 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
   oa.list_tmp = x.list_tmp;
   oa.cnt = x.cnt;
   oa.slot_bits = bits_for((uint64_t)(items - 1));
-  oa.kmag = k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)k + 1ull) : 0xFFFFFFFFu;
+  oa.sm = c.sm;
   oa.cmag = 0;
   oa.ents = flat_owner(c) ? x.ents : nullptr;
   oa.pieces = x.pieces;
@@ -2714,11 +2873,10 @@ static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
                                                                   m->steps_out, x.segs, x.heavy, c.items, m->state,
                                                                   c.B);
   WV_LAUNCH_CHECK();
-  group_place<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.V, x.cnt, x.list);
+  group_place<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.R, c.cw, c.V, x.cnt, x.list);
   WV_LAUNCH_CHECK();
   if (flat_owner(c)) {
-    const uint32_t kmag = c.k > 1 ? (uint32_t)(0xFFFFFFFFull / (uint64_t)c.k + 1ull) : 0xFFFFFFFFu;
-    group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, kmag);
+    group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, c.sm);
     WV_LAUNCH_CHECK();
     OwnerArgs oa = owner_args(c, h);
     const size_t smem = (size_t)heavy_bitmap_words(c.items) * 4;

@@ -309,6 +309,23 @@ class _DeviceCorpus:
         if self.n_pairs == 0:
             raise ValueError("empty training set")
 
+    def cbow_instances(self):
+        """CBOW instance table [N, 2W+1] int32 in the reference's order (w2v.py:194-222)."""
+        torch = self.torch
+        n = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        ws = torch.empty(_lib.query("wv_cbow_instances_workspace_bytes", self.n_walks), dtype=torch.uint8,
+                         device=self.dev)
+        st = _lib.stream_ptr()
+        _lib.call("wv_cbow_instances", _lib.ptr(self.tokens), _lib.ptr(self.offsets), self.n_walks, self.window, None,
+                  _lib.ptr(n), _lib.ptr(ws), ws.numel(), st)
+        self.n_instances = int(n.item())
+        if self.n_instances == 0:
+            raise ValueError("empty training set")
+        inst = torch.empty(self.n_instances * (2 * self.window + 1), dtype=torch.int32, device=self.dev)
+        _lib.call("wv_cbow_instances", _lib.ptr(self.tokens), _lib.ptr(self.offsets), self.n_walks, self.window,
+                  _lib.ptr(inst), _lib.ptr(n), _lib.ptr(ws), ws.numel(), st)
+        return inst
+
     def reference_pairs(self):
         """(N,2) int32 pair table in the reference's shift-major order (w2v.py:177-190)."""
         torch = self.torch
@@ -359,6 +376,21 @@ def generate_pairs(corpus, window_size: int, min_count: int, vocab_size: int | N
     return pairs, dc.freq.cpu().numpy()
 
 
+def generate_cbow_instances(corpus, window_size: int, min_count: int, vocab_size: int | None = None):
+    """(contexts (N, 2W) -1 padded, lengths, targets, frequency) like w2v.py:194-222, computed on the device."""
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if vocab_size is None:
+        tok, _, _, n_tok = _corpus_device_arrays(torch, dev, corpus)
+        vocab_size = int(tok[:n_tok].max()) + 1 if n_tok else 0
+    if vocab_size == 0:
+        raise ValueError("empty training set")
+    dc = _DeviceCorpus(torch, dev, corpus, vocab_size, window_size, min_count)
+    inst = dc.cbow_instances().view(-1, 2 * int(window_size) + 1).cpu().numpy().astype(np.int64)
+    ctx = inst[:, :-1]
+    return ctx, (ctx >= 0).sum(axis=1).astype(np.int64), inst[:, -1].copy(), dc.freq.cpu().numpy()
+
+
 # ---------------------------------------------------------------- trainer --
 class _Replica:
     """One worker: its parameter store, its batch workspace and launch closures.
@@ -375,18 +407,19 @@ class _Replica:
         torch = trainer.torch
         self.k = trainer.k
         self.batch_size = trainer.batch_size
+        self.cw = trainer.cbow_window
         self.ws = torch.empty(_lib.query("wv_sgns_batch_workspace_bytes", params.V, params.d, trainer.k,
-                                         trainer.batch_size, params.precision), dtype=torch.uint8,
+                                         trainer.batch_size, params.precision, self.cw), dtype=torch.uint8,
                               device=trainer.dev)
         _lib.call("wv_sgns_workspace_init", _lib.ptr(self.ws), self.ws.numel(), params.V, params.d, trainer.k,
-                  trainer.batch_size, params.precision, _lib.stream_ptr())
+                  trainer.batch_size, params.precision, self.cw, _lib.stream_ptr())
         self.graphs = {}
         self.graph_launches = {}  # key -> kernels per replay
         self.profile_samples = []  # [(decode, gather, group, owner, batch) ms] of profiled batches
         self.bind()
 
     def compatible(self, trainer) -> bool:
-        return trainer.k == self.k and trainer.batch_size <= self.batch_size
+        return trainer.k == self.k and trainer.batch_size <= self.batch_size and trainer.cbow_window == self.cw
 
     def retarget(self, trainer):
         """Train the same replica on another corpus (same batch geometry)."""
@@ -484,13 +517,16 @@ class _Trainer:
         self.config = config
         self.seed = int(rng_seed)
         self.events = events
-        self.k = int(config.negative_samples)
+        # CBOW draws window_size negatives per instance (w2v.py:481-484)
+        self.cbow_window = int(config.window_size) if config.model == CBOW else 0
+        self.k = int(config.window_size) if config.model == CBOW else int(config.negative_samples)
         self.pairs_mode = pairs
         self.graph_batches = int(graph_batches)
         self.profile = False
         self.V = int(vocab_size)
         self.dc = _DeviceCorpus(torch, self.dev, corpus, vocab_size, config.window_size, config.min_count)
-        self.N = self.dc.n_pairs
+        self.instances = self.dc.cbow_instances() if self.cbow_window else None
+        self.N = self.dc.n_instances if self.cbow_window else self.dc.n_pairs
         per_sample = estimate_per_sample_bytes(config.model, config.vector_size, config.negative_samples,
                                                config.window_size)
         budget = resolve_memory_budget(config)
@@ -498,7 +534,7 @@ class _Trainer:
         self.batch_size = _clamped_batch_size(bsz, per_sample, budget, config.memory_cap_fraction, events)
         self.precision = precision
         if pairs == "numpy":
-            self.ref_pairs = self.dc.reference_pairs()
+            self.ref_pairs = None if self.cbow_window else self.dc.reference_pairs()
             self.perm = torch.empty(self.N, dtype=torch.int64, device=self.dev)
             self.neg_table = torch.empty(max(self.N * self.k, 1), dtype=torch.int32, device=self.dev)
             self.h_candidates = np.flatnonzero(self.dc.keep.cpu().numpy() != 0).astype(np.int64)
@@ -508,13 +544,14 @@ class _Trainer:
         cand_identity = dc.n_candidates == self.V
         self.batch_struct = _lib.WvSgnsBatch(
             mode=_lib.PAIRS_EXPLICIT if pairs == "numpy" else _lib.PAIRS_NATIVE, negatives=self.k,
-            window=int(config.window_size), pad=0, batch_rows=self.batch_size, n_pairs=self.N,
+            window=int(config.window_size), model=_lib.MODEL_CBOW if self.cbow_window else _lib.MODEL_SKIPGRAM,
+            batch_rows=self.batch_size, n_pairs=self.N,
             seed=self.seed & 0xFFFFFFFFFFFFFFFF, tokens=_lib.ptr(dc.tokens), offsets=_lib.ptr(dc.offsets),
             walks_by_class=_lib.ptr(dc.walks_by_class), class_len=_lib.ptr(dc.class_len),
             class_walk_start=_lib.ptr(dc.class_walk_start), class_pair_start=_lib.ptr(dc.class_pair_start),
             n_classes=dc.n_classes, candidates=None if cand_identity else _lib.ptr(dc.candidates),
             n_candidates=dc.n_candidates, pairs=_lib.ptr(self.ref_pairs), perm=_lib.ptr(self.perm),
-            negative_table=_lib.ptr(self.neg_table))
+            negative_table=_lib.ptr(self.neg_table), instances=_lib.ptr(self.instances))
         if self.k > 0 and dc.n_candidates == 0:
             raise ValueError("no negative-sample candidates")
 
@@ -669,7 +706,7 @@ class _Trainer:
         """Batches per sync_interval_ms (w2v.py:628-639), from the HBM bytes one batch moves."""
         c = self.config
         es = 8 if self.precision == "fp64" else 4
-        rows = self.batch_size * (2 + self.k)
+        rows = self.batch_size * ((2 * self.cbow_window + 1 + self.k) if self.cbow_window else (2 + self.k))
         batch_bytes = rows * c.vector_size * es * 2 + min(rows, 2 * self.V) * c.vector_size * es * 8
         est_ms = max(batch_bytes / 3.0e12 * 1e3, 0.02)
         return max(1, min(int(round(c.sync_interval_ms / est_ms)), 1 << 14))
@@ -805,8 +842,6 @@ def train(corpus, vocab_size: int, config: TrainConfig, rng_seed: int, on_event=
       graph_batches  batches captured per CUDA graph
       exchange       a dist.RankExchange for multi-GPU data parallelism
     """
-    if config.model != SKIPGRAM:
-        raise NotImplementedError("the B200 backend implements model='skipgram' (CBOW is not on this path yet)")
     if precision not in ("fp32", "fp64"):
         raise ValueError("precision must be 'fp32' or 'fp64'")
     if pairs not in ("device", "numpy"):

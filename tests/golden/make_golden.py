@@ -167,6 +167,41 @@ def embeddings_and_train():
     np.savez_compressed(OUT / "w2v.npz", **out)
 
 
+def cbow():
+    """CBOW (w2v.py:194-222 instances, :302-361 gradients): instance tables and train() runs."""
+    from walkvec.w2v import generate_cbow_instances
+
+    out = {}
+    rng = np.random.default_rng(3)
+    seqs = [rng.integers(0, 12, size=int(rng.integers(1, 9))) for _ in range(60)]
+    lens = np.array([len(s) for s in seqs])
+    toks = np.concatenate(seqs)
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    corpus = walkvec.WalkCorpus(toks, offs, "random")
+    ctx, lengths, targets, freq = generate_cbow_instances(corpus, 3, 6, 12)
+    out["inst_tokens"], out["inst_offsets"] = toks, offs
+    out["inst_ctx"], out["inst_lengths"], out["inst_targets"], out["inst_freq"] = ctx, lengths, targets, freq
+    vocab, edges, g = rows_graph(random_rows(np.random.default_rng(21), 30, 150, 4))
+    c = random_walks(g, vocab.entity_tokens(), walk_depth=4, walk_number=6, rng_seed=4)
+    out["train_tokens"], out["train_offsets"], out["train_V"] = c.tokens, c.offsets, np.array(len(vocab))
+    cfgs = {
+        "sparse": dict(model="cbow", min_count=2, vector_size=12, epochs=2, window_size=3, learning_rate=0.02,
+                       batch_size=64),
+        "dense": dict(model="cbow", min_count=0, vector_size=8, epochs=1, window_size=2, learning_rate=0.01,
+                      batch_size=128, use_sparse=False),
+        "auto": dict(model="cbow", min_count=10, vector_size=16, epochs=1, window_size=5),
+        "multi": dict(model="cbow", min_count=0, vector_size=8, epochs=2, window_size=2, workers=2,
+                      reproducible=True, batch_size=16),
+    }
+    for name, kw in cfgs.items():
+        model, losses = train(c, len(vocab), TrainConfig(**kw), 42)
+        out[f"{name}_in"], out[f"{name}_out"] = model.input_matrix, model.output_matrix
+        out[f"{name}_losses"] = np.array(losses)
+        out[f"{name}_touched_in"], out[f"{name}_touched_out"] = model.touched_input, model.touched_output
+        out[f"{name}_cfg"] = np.array(json.dumps(kw))
+    np.savez_compressed(OUT / "cbow.npz", **out)
+
+
 def two_clique():
     rows = []
     for base in ("x", "y"):
@@ -207,11 +242,9 @@ def vocab_encoding():
 
 
 if __name__ == "__main__":
-    seedseq()
-    walks()
-    bfs()
-    embeddings_and_train()
-    two_clique()
-    vocab_encoding()
+    # python make_golden.py [generator ...]   (default: all)
+    gens = {f.__name__: f for f in (seedseq, walks, bfs, embeddings_and_train, two_clique, vocab_encoding, cbow)}
+    for name in (sys.argv[1:] or list(gens)):
+        gens[name]()
     for p in sorted(OUT.glob("*.np*")) + sorted(OUT.glob("*.json")):
         print(p.name, p.stat().st_size)

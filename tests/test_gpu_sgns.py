@@ -175,3 +175,47 @@ def test_pipelined_batches_equal_sequential(wv):
         out.append((sess.model.input_matrix, sess.model.output_matrix, losses))
     for a in out[1:]:
         assert np.array_equal(out[0][0], a[0]) and np.array_equal(out[0][1], a[1]) and out[0][2] == a[2]
+
+
+# ---------------------------------------------------------------- CBOW --
+def test_cbow_instances_match_reference(golden, wv):
+    g = golden("cbow.npz")
+    corpus = wv.WalkCorpus(g["inst_tokens"], g["inst_offsets"])
+    ctx, lens, tg, freq = wv.generate_cbow_instances(corpus, 3, 6, 12)
+    assert np.array_equal(ctx, g["inst_ctx"]) and np.array_equal(lens, g["inst_lengths"])
+    assert np.array_equal(tg, g["inst_targets"]) and np.array_equal(freq, g["inst_freq"])
+
+
+# fp64 replay of the reference's CBOW streams: 1e-10 absolute on parameters
+@pytest.mark.parametrize("name", ["sparse", "dense", "auto", "multi"])
+def test_cbow_replay_fp64_matches_reference(golden, wv, name):
+    g = golden("cbow.npz")
+    kw = json.loads(str(g[f"{name}_cfg"]))
+    corpus = wv.WalkCorpus(g["train_tokens"], g["train_offsets"])
+    model, losses = wv.train(corpus, int(g["train_V"]), wv.TrainConfig(**kw), 42, precision="fp64", pairs="numpy")
+    np.testing.assert_allclose(model.input_matrix, g[f"{name}_in"], rtol=0, atol=1e-10)
+    np.testing.assert_allclose(model.output_matrix, g[f"{name}_out"], rtol=0, atol=1e-10)
+    np.testing.assert_allclose(losses, g[f"{name}_losses"], rtol=1e-10)
+    assert np.array_equal(model.touched_input, g[f"{name}_touched_in"])
+    assert np.array_equal(model.touched_output, g[f"{name}_touched_out"])
+
+
+# fp32 store, same streams: 1e-4 absolute, loss 1e-5 relative
+def test_cbow_replay_fp32_within_tolerance(golden, wv):
+    g = golden("cbow.npz")
+    kw = json.loads(str(g["sparse_cfg"]))
+    corpus = wv.WalkCorpus(g["train_tokens"], g["train_offsets"])
+    model, losses = wv.train(corpus, int(g["train_V"]), wv.TrainConfig(**kw), 42, precision="fp32", pairs="numpy")
+    np.testing.assert_allclose(model.input_matrix, g["sparse_in"], rtol=0, atol=1e-4)
+    np.testing.assert_allclose(model.output_matrix, g["sparse_out"], rtol=0, atol=1e-4)
+    np.testing.assert_allclose(losses, g["sparse_losses"], rtol=1e-5)
+
+
+def test_cbow_device_mode_deterministic_and_learns(golden, wv):
+    g = golden("cbow.npz")
+    corpus = wv.WalkCorpus(g["train_tokens"], g["train_offsets"])
+    cfg = wv.TrainConfig(model="cbow", min_count=1, vector_size=16, epochs=4, window_size=3, batch_size=50)
+    a, la = wv.train(corpus, int(g["train_V"]), cfg, 3)
+    b, lb = wv.train(corpus, int(g["train_V"]), cfg, 3)
+    assert np.array_equal(a.input_matrix, b.input_matrix) and la == lb
+    assert la[-1] < la[0]

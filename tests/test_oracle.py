@@ -123,3 +123,28 @@ def test_two_clique_reference_statistics():
     runs = json.loads((GOLDEN / "two_clique.json").read_text())["runs"]
     m = np.array([r["margin"] for r in runs])
     assert len(runs) == 10 and m.min() > 0.3 and all(r["loss_last"] < r["loss0"] for r in runs)
+
+
+def test_cbow_instances_match_reference(golden):
+    g = golden("cbow.npz")
+    toks, offs = g["inst_tokens"], g["inst_offsets"]
+    freq = ov.frequencies(toks, 12)
+    assert np.array_equal(freq, g["inst_freq"])
+    ft, fo = ov.filtered(toks, offs, freq >= 6)
+    ctx, lens, tg = ov.cbow_instances(ft, fo, 3)
+    assert np.array_equal(ctx, g["inst_ctx"]) and np.array_equal(lens, g["inst_lengths"])
+    assert np.array_equal(tg, g["inst_targets"])
+
+
+@pytest.mark.parametrize("name", ["sparse", "dense", "auto"])
+def test_cbow_train_oracle_matches_reference(golden, name):
+    g = golden("cbow.npz")
+    kw = json.loads(str(g[f"{name}_cfg"]))
+    r = ov.train(g["train_tokens"], g["train_offsets"], int(g["train_V"]), kw["vector_size"], kw["window_size"],
+                 0, kw.get("learning_rate", 0.01), kw["min_count"], kw["epochs"], 42,
+                 batch=kw.get("batch_size"), sparse=kw.get("use_sparse", True), model="cbow")
+    np.testing.assert_allclose(r["inp"], g[f"{name}_in"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(r["out"], g[f"{name}_out"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(r["losses"], g[f"{name}_losses"], rtol=1e-12)
+    assert np.array_equal(r["touched_in"], g[f"{name}_touched_in"])
+    assert np.array_equal(r["touched_out"], g[f"{name}_touched_out"])
