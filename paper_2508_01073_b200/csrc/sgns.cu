@@ -327,22 +327,6 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
     const int jj = (int)(it - b * R);
     const int64_t pos = lo + b;
     int32_t* row = A.idx + b * R;
-    if (A.cw > 0) {
-      // CBOW: items 0..2W-1 the context rows (input side, -1 outside the walk),
-      // 2W the target and 2W+1.. the negatives (output side)
-      const int ctxw = 2 * A.cw;
-      if (jj <= ctxw) {
-        const int64_t q = D.mode == WV_PAIRS_NATIVE ? (int64_t)feistel_perm(fs, (uint64_t)pos, D.N) : D.perm[pos];
-        const int32_t t = D.inst[q * (ctxw + 1) + jj];
-        row[jj] = t;
-        if (t >= 0) group_claim(A, (uint32_t)t + (jj == ctxw ? (uint32_t)A.V : 0u));
-      } else {
-        const int32_t neg = draw_negative(D, pos, epoch, jj - ctxw - 1, k);
-        row[jj] = neg;
-        group_claim(A, (uint32_t)(neg + A.V));
-      }
-      continue;
-    }
     if (jj == 0) {
       int32_t center, context;
       if (D.mode == WV_PAIRS_NATIVE) {
@@ -373,7 +357,52 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       group_claim(A, (uint32_t)center);
       group_claim(A, (uint32_t)(context + A.V));
     } else if (jj >= 2) {
-      const int32_t neg = draw_negative(D, pos, epoch, jj - 2, k);
+      const int j = jj - 2;
+      int32_t neg;
+      if (D.mode == WV_PAIRS_NATIVE) {
+        // Philox4x32 counter (position, epoch, j/2): two draws per call
+        uint32_t rnd[4] = {(uint32_t)pos, (uint32_t)((uint64_t)pos >> 32), (uint32_t)epoch, (uint32_t)(j >> 1)};
+        philox4x32_10(rnd, (uint32_t)D.seed ^ 0xA5A5F00Du, (uint32_t)(D.seed >> 32) ^ 0x3C6EF372u);
+        const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
+        const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)D.n_candidates);
+        neg = D.candidates ? D.candidates[ci] : (int32_t)ci;
+      } else {
+        neg = D.negatives[pos * k + j];
+      }
+      row[jj] = neg;
+      group_claim(A, (uint32_t)(neg + A.V));
+    }
+  }
+}
+
+// CBOW decode, thread per item: items 0..2W-1 are the instance's context rows
+// (input side, -1 outside the walk), 2W the target and 2W+1.. the negatives
+// (output side); the instance is instances[perm(position)].
+__global__ void __launch_bounds__(128) cbow_decode_kernel(PairArgs A) {
+  __shared__ CorpusDesc D;
+  if (threadIdx.x == 0) D = *A.desc;
+  __syncthreads();
+  const int k = A.k;
+  const int R = A.R;
+  const int ctxw = 2 * A.cw;
+  const int64_t items = A.B * R;
+  const int64_t lo = A.state->lo;
+  const uint64_t epoch = (uint64_t)A.state->epoch;
+  Feistel fs;
+  if (D.mode == WV_PAIRS_NATIVE) fs = make_feistel(D.seed, epoch, D.N);
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = it / R;
+    const int jj = (int)(it - b * R);
+    const int64_t pos = lo + b;
+    int32_t* row = A.idx + b * R;
+    if (jj <= ctxw) {
+      const int64_t q = D.mode == WV_PAIRS_NATIVE ? (int64_t)feistel_perm(fs, (uint64_t)pos, D.N) : D.perm[pos];
+      const int32_t t = D.inst[q * (ctxw + 1) + jj];
+      row[jj] = t;
+      if (t >= 0) group_claim(A, (uint32_t)t + (jj == ctxw ? (uint32_t)A.V : 0u));
+    } else {
+      const int32_t neg = draw_negative(D, pos, epoch, jj - ctxw - 1, k);
       row[jj] = neg;
       group_claim(A, (uint32_t)(neg + A.V));
     }
@@ -1412,7 +1441,7 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
 #define WV_FLAT_U 1
 #endif
 #ifndef WV_FLAT_MINB
-#define WV_FLAT_MINB 4
+#define WV_FLAT_MINB 5
 #endif
 #ifndef WV_OWNER_FUSED_HEAVY
 #define WV_OWNER_FUSED_HEAVY 0
@@ -1598,7 +1627,7 @@ template <typename T, int EPC, int MAXC>
 #define WV_HEAVY_GRID (148 * 4)
 #endif
 #ifndef WV_OWNER_PER_SM
-#define WV_OWNER_PER_SM 3  // light-row owner CTAs per SM (room for the concurrent heavy pieces); 0: all resident
+#define WV_OWNER_PER_SM 4  // light-row owner CTAs per SM (room for the concurrent heavy pieces); 0: all resident
 #endif
 __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kernel(OwnerArgs A) {
   constexpr int W = kHeavyThreads / 32;
@@ -2812,7 +2841,10 @@ static int enqueue_decode(const BatchCtx& c, int h, cudaStream_t st) {
   WV_CUDA(cudaMemsetAsync(c.bw.half[h].gctr, 0, 8 * sizeof(uint32_t), st));
   if (flat_owner(c))
     WV_CUDA(cudaMemsetAsync(c.bw.half[h].rowdone, 0, (c.items / (kLightMax + 1) + 1) * 4, st));
-  sgns_decode_kernel<<<grid_for(c.items, 128, 148 * 32), 128, 0, st>>>(pa);
+  if (c.cw > 0)
+    cbow_decode_kernel<<<grid_for(c.items, 128, 148 * 32), 128, 0, st>>>(pa);
+  else
+    sgns_decode_kernel<<<grid_for(c.items, 128, 148 * 32), 128, 0, st>>>(pa);
   WV_LAUNCH_CHECK();
   return 0;
 }
