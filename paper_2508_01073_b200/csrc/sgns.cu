@@ -491,7 +491,10 @@ constexpr int kBulkThreads = kBulkWarps * 32;
 // CB = CBOW (w2v.py:302-361): the item is an instance whose up-to-2W context
 // rows are averaged into u = c (the masked mean), its target row takes the
 // positive logit, and the input-side gradient is grad_c / len.
-template <typename T, int EPC, int MAXC, bool CB, int NW>
+// KC > 0: the negative count is a compile-time constant (KC + 1 <= 8 dots):
+// the 1 + KC output rows are loaded from shared memory once into registers
+// and reused by the dots and the gradient row.
+template <typename T, int EPC, int MAXC, bool CB, int NW, int KC>
 __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, const T* __restrict__ in,
                                                                     const T* __restrict__ out) {
   constexpr int kBulkWarps = NW;
@@ -577,6 +580,61 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
         const int c = lane + 32 * q;
         if (c < C) u[q] = *reinterpret_cast<const Chunk<T, EPC>*>(rows + c * EPC);
       }
+    }
+    if constexpr (KC > 0) {
+      Chunk<T, EPC> x[KC + 1][MAXC];
+#pragma unroll
+      for (int t = 0; t <= KC; ++t)
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q) {
+          const int c = lane + 32 * q;
+          if (c < C) x[t][q] = *reinterpret_cast<const Chunk<T, EPC>*>(rows + (size_t)(ctxw + t) * d + c * EPC);
+        }
+      T part[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        part[t] = 0;
+        if (t <= KC) {
+#pragma unroll
+          for (int q = 0; q < MAXC; ++q) {
+            const int c = lane + 32 * q;
+            if (c < C) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) part[t] += u[q].v[e] * x[t][q].v[e];
+            }
+          }
+        }
+      }
+      const T red = warp_sum8(part);  // dot ((lane >> 2) & 7)
+      const T mydot = __shfl_sync(0xffffffffu, red, (lane & 7) << 2);
+      T mycoef = 0;
+      if (lane <= KC) {
+        loss_acc += (double)log1pexp_t<T>(lane == 0 ? -mydot : mydot);
+        const T sg = T(1) / (T(1) + exp_t(-mydot));
+        mycoef = (lane == 0 ? sg - T(1) : sg) * invB;
+        coef[b * (KC + 1) + lane] = mycoef;
+      }
+      T cf[KC + 1];
+#pragma unroll
+      for (int j = 0; j <= KC; ++j) cf[j] = __shfl_sync(0xffffffffu, mycoef, j);
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int c = lane + 32 * q;
+        if (c < C) {
+          Chunk<T, EPC> gg;
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) {
+            T acc = 0;
+#pragma unroll
+            for (int j = 1; j <= KC; ++j) acc = mad_t(cf[j], x[j][q].v[e], acc);
+            gg.v[e] = mad_t(cf[0], x[0][q].v[e], acc);
+          }
+          st_chunk<T, EPC>(G + b * d + c * EPC, gg);
+          st_chunk<T, EPC>(U + b * d + c * EPC, u[q]);
+        }
+      }
+      __syncwarp();
+      continue;
     }
     // dot j = <u, row ctxw+j> (j = 0: context / target, j >= 1: negative j-1),
     // eight at a time through one transposed butterfly; lane j ends up holding dot j
@@ -2250,9 +2308,9 @@ static inline size_t bulk_smem_bytes(int nw, int d, int R, size_t es) {
 static constexpr size_t kBulkSmemMax = 220 * 1024;
 
 // one bulk-gather instantiation: smem attribute, persistent grid of resident CTAs
-template <typename T, int EPC, int MAXC, bool CB, int NW>
+template <typename T, int EPC, int MAXC, bool CB, int NW, int KC = 0>
 static int launch_bulk_gather(const PairArgs& a, const void* in, const void* out, size_t smem, cudaStream_t st) {
-  auto kern = sgns_gather_bulk_kernel<T, EPC, MAXC, CB, NW>;
+  auto kern = sgns_gather_bulk_kernel<T, EPC, MAXC, CB, NW, KC>;
   static size_t attr_set[16] = {0};
   static int resident[16] = {0};
   static size_t resident_smem[16] = {0};
@@ -2301,8 +2359,10 @@ struct LaunchPair {
       return -1;
     }
     const size_t smem = bulk_smem_bytes(kBulkWarps, a.d, 2 + a.k, sizeof(T));
-    if (rows16 && smem <= kBulkSmemMax && getenv("WV_SGNS_REG_GATHER") == nullptr)
+    if (rows16 && smem <= kBulkSmemMax && getenv("WV_SGNS_REG_GATHER") == nullptr) {
+      if (a.k == 5) return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps, 5>(a, in, out, smem, st);
       return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps>(a, in, out, smem, st);
+    }
     sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
     WV_LAUNCH_CHECK();
     return 0;
