@@ -892,10 +892,19 @@ struct Segment {
   double bc2;
 };
 
+// RowAdam bias corrections 1 - b1^t, 1 - b2^t for t < kBcTable, computed once
+// per device with the same pow as the fallback (a table load replaces two
+// float64 pow calls per unique row)
+constexpr int kBcTable = 1 << 16;
+__global__ void fill_bc_table(double2* tab) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < kBcTable) tab[t] = make_double2(1.0 - pow(0.9, (double)t), 1.0 - pow(0.999, (double)t));
+}
+
 __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __restrict__ cnt, uint32_t* gctr,
                                int64_t V, int sparse, int32_t* __restrict__ steps_in, int32_t* __restrict__ steps_out,
                                Segment* __restrict__ segs, Segment* __restrict__ heavy, int64_t max_unique,
-                               WvSgnsDevState* state, int64_t B) {
+                               WvSgnsDevState* state, int64_t B, const double2* __restrict__ bc_table) {
   const int lane = threadIdx.x & 31;
   // the batch's pairs are decoded: advance the decode cursor for the next batch
   if (blockIdx.x == 0 && threadIdx.x == 0) state->lo += B;
@@ -939,8 +948,14 @@ __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __re
         const int64_t row = side_out ? (int64_t)key - V : (int64_t)key;
         const int t = steps[row] + 1;
         steps[row] = t;
-        sg.bc1 = 1.0 - pow(0.9, (double)t);
-        sg.bc2 = 1.0 - pow(0.999, (double)t);
+        if (t < kBcTable) {
+          const double2 bc = bc_table[t];
+          sg.bc1 = bc.x;
+          sg.bc2 = bc.y;
+        } else {
+          sg.bc1 = 1.0 - pow(0.9, (double)t);
+          sg.bc2 = 1.0 - pow(0.999, (double)t);
+        }
       }
       const uint32_t below = (1u << lane) - 1u;
       if (is_heavy)
@@ -976,6 +991,39 @@ __global__ void group_place(const int32_t* __restrict__ idx, int64_t B, int k, i
       slot = (uint32_t)(j < ctxw ? b * ctxw + j : (j == ctxw ? b : B + b * k + (j - ctxw - 1)));
     }
     list[atomicAdd(cnt + key, 1u)] = slot;
+  }
+}
+
+// group_place with the atomics of equal keys inside a warp merged (hot rows:
+// predicates and hubs take ~100 contributions per batch): one atomic per
+// distinct key per warp, lanes take consecutive list positions
+__global__ void group_place_agg(const int32_t* __restrict__ idx, int64_t B, int k, int R, int cw, int64_t V,
+                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
+  const int64_t items = B * R;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < items; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint32_t key = 0xffffffffu, slot = 0;
+    if (i < items) {
+      const int64_t b = i / R;
+      const int j = (int)(i - b * R);
+      const int32_t t = idx[i];
+      if (cw == 0) {
+        key = (uint32_t)t + (j == 0 ? 0u : (uint32_t)V);
+        slot = (uint32_t)(j == 0 ? b : (j == 1 ? B + b : 2 * B + b * k + (j - 2)));
+      } else if (t >= 0) {
+        const int ctxw = 2 * cw;
+        key = (uint32_t)t + (j < ctxw ? 0u : (uint32_t)V);
+        slot = (uint32_t)(j < ctxw ? b * ctxw + j : (j == ctxw ? b : B + b * k + (j - ctxw - 1)));
+      }
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    uint32_t pos = 0;
+    if (lane == leader && key != 0xffffffffu) pos = atomicAdd(cnt + key, (uint32_t)__popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (key != 0xffffffffu) list[pos + rank] = slot;
   }
 }
 
@@ -2254,6 +2302,28 @@ static inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 32) 
 
 static inline int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
 
+// per-device bias-correction table (built outside any graph capture: at
+// workspace init, or on first use by an uncaptured batch)
+static double2* g_bc_table[16] = {nullptr};
+static cudaError_t bc_table(double2** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  if (g_bc_table[dev] == nullptr) {
+    double2* t = nullptr;
+    e = cudaMalloc(&t, sizeof(double2) * kBcTable);
+    if (e != cudaSuccess) return e;
+    fill_bc_table<<<kBcTable / 256, 256>>>(t);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+    g_bc_table[dev] = t;
+  }
+  *out = g_bc_table[dev];
+  return cudaSuccess;
+}
+
 static uint64_t g_sg_table_ready = 0;
 static cudaError_t ensure_sg_table() {
   int dev = 0;
@@ -2389,8 +2459,20 @@ static cudaError_t side_stream(SideStream** out) {
   if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
   SideStream& ss = tab[dev];
   if (ss.s == nullptr) {
-    e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ss.h, cudaStreamNonBlocking);
+    // the side stream (next batch's decode + grouping) gets the highest priority so
+    // its CTAs take SM slots as soon as any free up during the current batch
+    int lo_prio = 0, hi_prio = 0;
+    e = cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+#ifndef WV_SIDE_PRIO
+#define WV_SIDE_PRIO 1
+#endif
+#ifndef WV_HEAVY_PRIO
+#define WV_HEAVY_PRIO 0
+#endif
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, WV_SIDE_PRIO ? hi_prio : lo_prio);
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&ss.h, cudaStreamNonBlocking, WV_HEAVY_PRIO ? hi_prio : lo_prio);
     cudaEvent_t* evs[] = {&ss.fork, &ss.join, &ss.fork_h, &ss.join_h, &ss.dec[0], &ss.dec[1],
                           &ss.grp[0], &ss.grp[1], &ss.own[0], &ss.own[1]};
     for (cudaEvent_t* ev : evs)
@@ -2798,6 +2880,8 @@ int wv_sgns_workspace_init(void* ws, int64_t ws_bytes, int64_t vocab_size, int v
                                       rows_per_item(negatives, cbow_window), batch, precision == WV_FP64 ? 8 : 4, bw);
   WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
   for (int h = 0; h < 2; ++h) WV_CUDA(cudaMemsetAsync(bw.half[h].cnt, 0, 2 * vocab_size * 4, (cudaStream_t)stream));
+  double2* bct = nullptr;
+  WV_CUDA(bc_table(&bct));  // before any CUDA-graph capture of batches
   return 0;
 }
 
@@ -2961,11 +3045,13 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
 static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
   const BatchHalf& x = c.bw.half[h];
   const WvSgnsModel* m = c.model;
+  double2* bct = nullptr;
+  WV_CUDA(bc_table(&bct));
   group_segments<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.uniq, x.cnt, x.gctr, c.V, m->sparse, m->steps_in,
                                                                   m->steps_out, x.segs, x.heavy, c.items, m->state,
-                                                                  c.B);
+                                                                  c.B, bct);
   WV_LAUNCH_CHECK();
-  group_place<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.R, c.cw, c.V, x.cnt, x.list);
+  group_place_agg<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.R, c.cw, c.V, x.cnt, x.list);
   WV_LAUNCH_CHECK();
   if (flat_owner(c)) {
     group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, c.sm);
@@ -2979,7 +3065,10 @@ static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
       WV_CUDA(cudaFuncSetAttribute(heavy_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr[dev] = smem;
     }
-    heavy_order<<<148 * 2, kHeavyThreads, smem, st>>>(oa, x.gctr, x.pieces);
+    // enough CTAs for every heavy row in one round (rows beyond exit at once)
+    const int64_t max_heavy = c.items / (kLightMax + 1) + 1;
+    heavy_order<<<(unsigned)(max_heavy < 148 * 8 ? max_heavy : 148 * 8), kHeavyThreads, smem, st>>>(oa, x.gctr,
+                                                                                                  x.pieces);
     WV_LAUNCH_CHECK();
   }
   return 0;
@@ -3133,24 +3222,31 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
   WV_CHECK_ARG(count >= 1, "count must be >= 1");
   BatchCtx c;
   WV_CUDA_RC(batch_ctx(model, batch, ws, ws_bytes, c));
-  c.timer = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   WV_CUDA_RC(bind_if_eager(batch, c, st));
   SideStream* ss = nullptr;
   WV_CUDA(side_stream(&ss));
   WV_CUDA(cudaEventRecord(ss->fork, st));
   WV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  // optional timeline (profiling): per batch i, slots timer_base + 5i + {0 side start,
+  // 1 side end, 2 gather start, 3 gather end, 4 update end}
   for (int64_t i = 0; i < count; ++i) {
     const int h = (int)(i & 1);
+    const int t0 = 5 * (int)i;
     if (i >= 2) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[h], 0));
+    WV_STAMP(t0 + 0, ss->s);
     WV_CUDA_RC(enqueue_decode(c, h, ss->s));
     WV_CUDA(cudaEventRecord(ss->dec[h], ss->s));
     WV_CUDA_RC(enqueue_group(c, h, ss->s));
+    WV_STAMP(t0 + 1, ss->s);
     WV_CUDA(cudaEventRecord(ss->grp[h], ss->s));
     WV_CUDA(cudaStreamWaitEvent(st, ss->dec[h], 0));
+    WV_STAMP(t0 + 2, st);
     WV_CUDA_RC(enqueue_gather(c, h, st));
+    WV_STAMP(t0 + 3, st);
     WV_CUDA(cudaStreamWaitEvent(st, ss->grp[h], 0));
     WV_CUDA_RC(enqueue_update(c, h, ss, st));
+    WV_STAMP(t0 + 4, st);
     WV_CUDA(cudaEventRecord(ss->own[h], st));
   }
   WV_CUDA(cudaEventRecord(ss->join, ss->s));
