@@ -113,8 +113,12 @@ struct Walker {
 // hop loop interleaves the thread's walkers so their dependent CSR reads
 // (offsets -> packed edge) overlap.  Rows are staged in shared memory and
 // written with 16-byte stores.
+#ifndef WV_WALK_MINB
+#define WV_WALK_MINB 1
+#endif
 template <int RNG, int WPT>
-__global__ void __launch_bounds__(kWalkThreads) random_walk_kernel(WalkParams P, const PcgJump* __restrict__ jrows) {
+__global__ void __launch_bounds__(kWalkThreads, WV_WALK_MINB) random_walk_kernel(WalkParams P,
+                                                                              const PcgJump* __restrict__ jrows) {
   extern __shared__ int32_t stage[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = P.width;
@@ -147,7 +151,6 @@ __global__ void __launch_bounds__(kWalkThreads) random_walk_kernel(WalkParams P,
     // walker q of this thread: sub-block q, so each warp's 32 walkers are consecutive
     const int64_t wl = blk0 + (int64_t)q * kWalkThreads + threadIdx.x;
     int32_t* my = stage + ((q * kWalkThreads) + warp * 32 + lane) * width;
-    for (int j = 0; j < width; ++j) my[j] = -1;
     W[q].alive = wl < P.work_count;
     W[q].len = 0;
     W[q].cur = 0;
@@ -226,6 +229,9 @@ __global__ void __launch_bounds__(kWalkThreads) random_walk_kernel(WalkParams P,
   for (int q = 0; q < WPT; ++q) {
     const int64_t wl = blk0 + (int64_t)q * kWalkThreads + threadIdx.x;
     if (wl < P.work_count) P.lengths[wl] = W[q].len;
+    // pad the staged row past the walk's end (-1, the reference's PAD)
+    int32_t* my = stage + ((q * kWalkThreads) + warp * 32 + lane) * width;
+    for (int j = W[q].len; j < width; ++j) my[j] = -1;
   }
   __syncwarp();
 #pragma unroll

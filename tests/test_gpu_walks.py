@@ -175,3 +175,39 @@ def test_bfs_cap_is_prefix_and_large_trees(wv):
     capped, _ = wv.bfs_walks(graph, roots, 4, max_walks_per_root=250)
     tok, offs, _ = ow.bfs_walks(off, tgt, prd, roots, 4, cap=250)
     assert np.array_equal(capped.tokens, tok) and np.array_equal(capped.offsets, offs)
+
+
+def test_cfg3_bfs_capped_on_cfg2_graph_bit_exact(wv):
+    """BASELINE cfg3: BFS depth 4, <= 250 walks per entity on the 1M-entity cfg2 graph
+    (device-generated BA(1M, m=10), 200 predicates); 2,000 uniformly sampled roots bit-exact
+    against the oracle, walks and PathTable."""
+    from paper_2508_01073_b200 import synth
+
+    edges, V, ents, _ = synth.device_synthetic_kg("barabasi", 1_000_000, m=10, predicates=200, seed=7)
+    graph = wv.build_graph(edges, V)
+    off, tgt, prd = graph.row_offsets, graph.col_targets, graph.col_predicates
+    ents = ents.cpu().numpy()
+    roots = np.random.default_rng(5).choice(ents, 2000, replace=False)
+    corpus, table = wv.bfs_walks(graph, roots, 4, max_walks_per_root=250)
+    tok, offs, rows = ow.bfs_walks(off, tgt, prd, roots, 4, cap=250)
+    assert np.array_equal(corpus.tokens, tok) and np.array_equal(corpus.offsets, offs)
+    assert np.array_equal(np.array(table.rows(), dtype=np.int64).reshape(-1, 3), np.asarray(rows, dtype=np.int64).reshape(-1, 3))
+
+
+def test_cfg4_er_long_walks_shards_bit_exact(wv):
+    """BASELINE cfg4 shape: ER(15,000, p=0.001378) with 237 predicates, walks
+    depth 16 x 500 per entity (7.5M walks, all 33 tokens); sampled shards bit-exact."""
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("erdos_renyi", 15_000, p=0.001378, predicates=237, seed=7)
+    assert 300_000 < len(edges) < 320_000
+    graph = wv.build_graph(edges, V)
+    c = wv.random_walks(graph, ents, walk_depth=16, walk_number=500, rng_seed=42)
+    assert len(c) == len(ents) * 500
+    off, tgt, prd = ow.csr(edges, V)
+    n_sh = -(-len(ents) * 500 // ow.SHARD)
+    for s in (0, n_sh // 2, n_sh - 1):
+        tok, offs = ow.random_walks(off, tgt, prd, ents, 16, 500, 42, "pcg64", shards=[s])
+        w0 = s * ow.SHARD
+        lo, hi = c.offsets[w0], c.offsets[min(w0 + ow.SHARD, len(c))]
+        assert np.array_equal(c.tokens[lo:hi], tok)
