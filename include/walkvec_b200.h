@@ -244,6 +244,32 @@ int wv_cbow_instances(const int32_t* tokens, const int64_t* offsets, int64_t n_w
  * one CUDA graph.  Replaces the batch loop of w2v._train_single (w2v.py:553-565). */
 int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes, int64_t count,
                     void* stream);
+/* ----------------------------------------------------------- row-sharded --
+ * cfg5 mode (SGNS state too large to replicate): rank `shard` of
+ * `nshard` owns rows r with r % nshard == shard of both matrices (local row
+ * r / nshard) and their RowAdam state; `model` is that local store
+ * (vocab_size = ceil(vocab_global / nshard)).  Per global batch:
+ * decode_group -> requests -> (all-to-all) -> serve -> (all-to-all) -> place ->
+ * gather -> (all-gather of U, G, coef in global pair order) -> update.  The
+ * result equals single-GPU training with the same global batch. */
+int wv_shard_init(int64_t vocab_global, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
+                  int nshard, int shard, void* input_local, void* output_local, void* stream);
+int wv_shard_decode_group(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                          int64_t vocab_global, int nshard, int shard, void* stream);
+int wv_shard_requests(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                      int64_t vocab_global, int nshard, int shard, int64_t item_begin, int64_t n_items,
+                      uint32_t* cursor, int64_t* keys, int32_t* items, int32_t* ident, int64_t* counts,
+                      void* stream);
+int wv_shard_serve(const WvSgnsModel* model, const int64_t* keys, int64_t n, int64_t vocab_global, int nshard,
+                   void* rows, void* stream);
+int wv_shard_place(const void* rows, const int32_t* items, int64_t n, int vector_size, int precision,
+                   void* itemrows, void* stream);
+int wv_shard_gather(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                    int64_t vocab_global, int nshard, int shard, const void* itemrows, const int32_t* ident,
+                    int64_t pair_count, void* U, void* G, void* coef, void* stream);
+int wv_shard_update(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                    int64_t vocab_global, int nshard, int shard, const void* U, const void* G, const void* coef,
+                    void* stream);
 #define WV_PHASE_PAIRS 1  /* decode pair/negative rows; gather rows, dots, coefficients, batch loss */
 #define WV_PHASE_GROUP 2  /* group contribution slots by destination row (no sort) */
 #define WV_PHASE_UPDATE 4 /* per unique row: slot-ordered sum + RowAdam */

@@ -158,6 +158,13 @@ SIGNATURES = {
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
     "wv_sgns_batches": (I32, [P, P, P, I64, I64, P]),
+    "wv_shard_init": (I32, [I64, I32, P, I32, I32, I32, I32, P, P, P]),
+    "wv_shard_decode_group": (I32, [P, P, P, I64, I64, I32, I32, P]),
+    "wv_shard_requests": (I32, [P, P, P, I64, I64, I32, I32, I64, I64, P, P, P, P, P, P]),
+    "wv_shard_serve": (I32, [P, P, I64, I64, I32, P, P]),
+    "wv_shard_place": (I32, [P, P, I64, I32, I32, P, P]),
+    "wv_shard_gather": (I32, [P, P, P, I64, I64, I32, I32, P, P, I64, P, P, P, P]),
+    "wv_shard_update": (I32, [P, P, P, I64, I64, I32, I32, P, P, P, P]),
     "wv_replica_delta": (I32, [P, P, I64, I32, P, P]),
     "wv_replica_apply": (I32, [P, P, P, P, I64, I32, I32, P]),
     "wv_barabasi_edge_count": (I64, [I64, I32]),

@@ -258,6 +258,10 @@ struct PairArgs {
   int R;   // rows per item: 2 + k (skip-gram) or 2W + 1 + k (CBOW)
   int cw;  // CBOW window W (0: skip-gram)
   int64_t B;  // rows in this batch
+  int64_t Bn;     // gradient normaliser (rows of the global batch; 0: B)
+  int nshard;     // row-sharded mode: this rank claims rows r with r % nshard == shard
+  int shard;
+  int64_t Vl;     // local rows per matrix (key space of the claims: [0, 2 Vl))
   const CorpusDesc* desc;
   // outputs
   void* U;
@@ -287,8 +291,23 @@ struct PairArgs {
 // deterministic, and reset cnt[key] to 0 for the next batch.
 enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3, GC_PIECES = 4 };
 
+// global row key (row, or V + row) -> local key of this rank, false if another rank owns it
+__device__ __forceinline__ bool owned_key(uint32_t key, int64_t V, int nshard, int shard, int64_t Vl, uint32_t& lk) {
+  if (nshard <= 1) {
+    lk = key;
+    return true;
+  }
+  const bool side = key >= (uint32_t)V;
+  const uint32_t row = side ? key - (uint32_t)V : key;
+  if ((int)(row % (uint32_t)nshard) != shard) return false;
+  lk = row / (uint32_t)nshard + (side ? (uint32_t)Vl : 0u);
+  return true;
+}
+
 __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
-  if (atomicAdd(A.cnt + key, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = key;
+  uint32_t lk;
+  if (!owned_key(key, A.V, A.nshard, A.shard, A.Vl, lk)) return;
+  if (atomicAdd(A.cnt + lk, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = lk;
 }
 
 // Phase 1a, thread per item: the batch's row indices (centre, context, k
@@ -518,7 +537,7 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
   T* U = (T*)A.U;
   T* G = (T*)A.G;
   T* coef = (T*)A.coef;
-  const T invB = (T)1 / (T)B;
+  const T invB = (T)1 / (T)(A.Bn > 0 ? A.Bn : B);
   const int64_t stride = (int64_t)gridDim.x * kBulkWarps;
   int64_t b = blockIdx.x * (int64_t)kBulkWarps + warp;
   auto issue = [&](int64_t pb, int stage) {
@@ -998,7 +1017,8 @@ __global__ void group_place(const int32_t* __restrict__ idx, int64_t B, int k, i
 // predicates and hubs take ~100 contributions per batch): one atomic per
 // distinct key per warp, lanes take consecutive list positions
 __global__ void group_place_agg(const int32_t* __restrict__ idx, int64_t B, int k, int R, int cw, int64_t V,
-                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ list) {
+                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ list, int nshard, int shard,
+                                int64_t Vl) {
   const int64_t items = B * R;
   const int lane = threadIdx.x & 31;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < items; base += (int64_t)gridDim.x * blockDim.x) {
@@ -1016,6 +1036,10 @@ __global__ void group_place_agg(const int32_t* __restrict__ idx, int64_t B, int 
         key = (uint32_t)t + (j < ctxw ? 0u : (uint32_t)V);
         slot = (uint32_t)(j < ctxw ? b * ctxw + j : (j == ctxw ? b : B + b * k + (j - ctxw - 1)));
       }
+    }
+    if (key != 0xffffffffu && nshard > 1) {
+      uint32_t lk;
+      key = owned_key(key, V, nshard, shard, Vl, lk) ? lk : 0xffffffffu;
     }
     const uint32_t peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
@@ -2293,6 +2317,88 @@ __global__ void scatter_candidates(const uint8_t* __restrict__ keep, const int64
     if (keep[i]) cand[pos[i]] = (int32_t)i;
 }
 
+// ------------------------------------------------------- row-sharded --
+// Init of the rows this rank owns (global row l * nshard + shard -> local l),
+// the same PCG64 elements as init_rows.
+template <typename T>
+__global__ void init_rows_shard(InitStream g0, int64_t V, int d, int64_t Vl, int nshard, int shard, int matrix,
+                                T* __restrict__ dst) {
+  const double bound = 1.0 / (double)d;
+  const double lower = -bound, range = bound - (-bound);
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < Vl; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = l * nshard + shard;
+    if (row >= V) {
+      for (int c = 0; c < d; ++c) dst[l * d + c] = (T)0;
+      continue;
+    }
+    const uint64_t k0 = (uint64_t)matrix * (uint64_t)V * d + (uint64_t)row * d;
+    PcgJump j = jump_sg(k0 + 1);
+    u128 x = add128(mul128(j.A, g0.state), mul128(g0.inc, j.S));
+    const u128 a1{PCG_MULT_LO, PCG_MULT_HI};
+    for (int c = 0; c < d; ++c) {
+      const double u = u64_to_double(pcg_output(x));
+      dst[l * d + c] = (T)__dadd_rn(lower, __dmul_rn(range, u));
+      x = add128(mul128(a1, x), g0.inc);
+    }
+  }
+}
+
+// Row requests of this rank's pairs, grouped by owner: pass 0 counts, pass 1
+// places (global key = row or V + row, local item index).  ident[i] = item
+// index, or -1 for a masked CBOW context column (no row).
+__global__ void shard_requests(const int32_t* __restrict__ idx, int64_t item_begin, int64_t n_items, int R, int ctxw,
+                               int64_t V, int nshard, int pass, uint32_t* __restrict__ cursor,
+                               int64_t* __restrict__ keys, int32_t* __restrict__ items,
+                               int32_t* __restrict__ ident) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_items; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = item_begin + i;
+    const int j = (int)(gi % R);
+    const int32_t t = idx[gi];
+    if (pass == 1) ident[i] = t >= 0 ? (int32_t)i : -1;
+    if (t < 0) continue;
+    const int owner = (int)((uint32_t)t % (uint32_t)nshard);
+    const uint32_t at = atomicAdd(cursor + owner, 1u);
+    if (pass == 1) {
+      keys[at] = (int64_t)t + (j < ctxw ? 0 : V);
+      items[at] = (int32_t)i;
+    }
+  }
+}
+
+__global__ void shard_offsets(uint32_t* cursor, int nshard, int64_t* counts) {
+  // cursor[0..n) holds counts after pass 0: copy them out, turn the cursor into offsets
+  uint32_t run = 0;
+  for (int o = 0; o < nshard; ++o) {
+    const uint32_t c = cursor[o];
+    counts[o] = c;
+    cursor[o] = run;
+    run += c;
+  }
+}
+
+template <typename T>
+__global__ void shard_serve(const T* __restrict__ in, const T* __restrict__ out, const int64_t* __restrict__ keys,
+                            int64_t n, int64_t V, int nshard, int d, T* __restrict__ rows) {
+  const int C = d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * C; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = i / C;
+    const int c = (int)(i - q * C);
+    const int64_t key = keys[q];
+    const bool side = key >= V;
+    const int64_t local = (side ? key - V : key) / nshard;
+    rows[i] = (side ? out : in)[local * d + c];
+  }
+}
+
+template <typename T>
+__global__ void shard_place(const T* __restrict__ rows, const int32_t* __restrict__ items, int64_t n, int d,
+                            T* __restrict__ itemrows) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * d; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = i / d;
+    itemrows[(int64_t)items[q] * d + (i - q * d)] = rows[i];
+  }
+}
+
 static inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -2915,6 +3021,8 @@ struct BatchCtx {
   int d, k;
   int R, cw;  // rows per item, CBOW window (0: skip-gram)
   SlotMap sm;
+  int64_t Vtok;       // token space of the corpus (V unless row-sharded)
+  int nshard, shard;  // row-sharded mode (1, 0 otherwise)
   BatchWs bw;
   void* timer;
   int tb;
@@ -2946,17 +3054,24 @@ static int batch_ctx(const WvSgnsModel* model, const WvSgnsBatch* batch, void* w
   WV_CHECK_ARG(ws_bytes >= need, "workspace too small");
   c.timer = batch->timer;
   c.tb = (int)batch->timer_base;
+  c.Vtok = c.V;
+  c.nshard = 1;
+  c.shard = 0;
   return 0;
 }
 
 static PairArgs pair_args(const BatchCtx& c, int h) {
   PairArgs pa;
-  pa.V = c.V;
   pa.d = c.d;
   pa.k = c.k;
   pa.R = c.R;
   pa.cw = c.cw;
   pa.B = c.B;
+  pa.Bn = 0;
+  pa.nshard = c.nshard;
+  pa.shard = c.shard;
+  pa.Vl = c.V;
+  pa.V = c.Vtok;
   pa.desc = c.bw.desc;
   pa.U = c.bw.U;
   pa.G = c.bw.G;
@@ -3051,7 +3166,8 @@ static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
                                                                   m->steps_out, x.segs, x.heavy, c.items, m->state,
                                                                   c.B, bct);
   WV_LAUNCH_CHECK();
-  group_place_agg<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.R, c.cw, c.V, x.cnt, x.list);
+  group_place_agg<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.R, c.cw, c.Vtok, x.cnt, x.list,
+                                                                   c.nshard, c.shard, c.V);
   WV_LAUNCH_CHECK();
   if (flat_owner(c)) {
     group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, c.sm);
@@ -3253,6 +3369,166 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
   WV_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
   return 0;
 }
+
+// ---------------------------------------------------------- row-sharded --
+// cfg5 mode: rank `shard` of `nshard` owns the rows r with
+// r % nshard == shard of both matrices (local row r / nshard) plus their
+// RowAdam state; `model` describes that local store (vocab_size = ceil(V /
+// nshard)), `vocab_global` is V.  One global batch (batch->batch_rows pairs):
+//   wv_shard_decode_group   every rank decodes the whole batch and groups
+//                           the contribution slots of its own rows
+//   wv_shard_requests       row requests of the rank's share of pairs, by owner
+//   (caller: all-to-all of the requests)   wv_shard_serve: rows for them
+//   (caller: all-to-all back)              wv_shard_place: rows -> item order
+//   wv_shard_gather         the rank's pairs: loss, coefficients, U/G rows
+//   (caller: all-gather of U, G, coef into global-batch order)
+//   wv_shard_update         slot-ordered sums + RowAdam on the rank's rows
+// The result equals single-GPU training with the same global batch size.
+
+static int shard_ctx(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                     int64_t vocab_global, int nshard, int shard, wv::BatchCtx& c) {
+  using namespace wv;
+  WV_CHECK_ARG(nshard >= 1 && shard >= 0 && shard < nshard, "bad shard %d of %d", shard, nshard);
+  WV_CHECK_ARG(model->vocab_size == (vocab_global + nshard - 1) / nshard, "local store must hold ceil(V / nshard) rows");
+  WV_CHECK_ARG(model->sparse, "row-sharded training implements sparse RowAdam");
+  WV_CUDA_RC(batch_ctx(model, batch, ws, ws_bytes, c));
+  WV_CHECK_ARG(flat_owner(c), "row-sharded training needs the flat owner path");
+  c.Vtok = vocab_global;
+  c.nshard = nshard;
+  c.shard = shard;
+  return 0;
+}
+
+int wv_shard_init(int64_t vocab_global, int vector_size, const uint32_t* seed_prefix, int n_prefix, int precision,
+                  int nshard, int shard, void* input_local, void* output_local, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(nshard >= 1 && shard >= 0 && shard < nshard, "bad shard");
+  WV_CUDA(ensure_sg_table());
+  uint32_t pool[4];
+  ss_pool(seed_prefix, n_prefix - 1, seed_prefix[n_prefix - 1], pool);
+  Pcg64 g = pcg_seed(pool);
+  InitStream sg{g.state, g.inc};
+  const int64_t Vl = (vocab_global + nshard - 1) / nshard;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int mtx = 0; mtx < 2; ++mtx) {
+    void* dst = mtx == 0 ? input_local : output_local;
+    if (precision == WV_FP32)
+      init_rows_shard<float><<<grid_for(Vl, 128), 128, 0, st>>>(sg, vocab_global, vector_size, Vl, nshard, shard, mtx,
+                                                                 (float*)dst);
+    else
+      init_rows_shard<double><<<grid_for(Vl, 128), 128, 0, st>>>(sg, vocab_global, vector_size, Vl, nshard, shard,
+                                                                  mtx, (double*)dst);
+    WV_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+int wv_shard_decode_group(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                          int64_t vocab_global, int nshard, int shard, void* stream) {
+  using namespace wv;
+  BatchCtx c;
+  WV_CUDA_RC(shard_ctx(model, batch, ws, ws_bytes, vocab_global, nshard, shard, c));
+  cudaStream_t st = (cudaStream_t)stream;
+  WV_CUDA_RC(bind_if_eager(batch, c, st));
+  WV_CUDA_RC(enqueue_decode(c, 0, st));
+  return enqueue_group(c, 0, st);
+}
+
+// requests of items [item_begin, item_begin + n_items) of the decoded batch;
+// keys/items (sized n_items) come out grouped by owner, counts[nshard] (device
+// int64) per owner; cursor is device scratch of nshard u32
+int wv_shard_requests(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                      int64_t vocab_global, int nshard, int shard, int64_t item_begin, int64_t n_items,
+                      uint32_t* cursor, int64_t* keys, int32_t* items, int32_t* ident, int64_t* counts,
+                      void* stream) {
+  using namespace wv;
+  BatchCtx c;
+  WV_CUDA_RC(shard_ctx(model, batch, ws, ws_bytes, vocab_global, nshard, shard, c));
+  cudaStream_t st = (cudaStream_t)stream;
+  WV_CUDA(cudaMemsetAsync(cursor, 0, nshard * 4, st));
+  const int ctxw = c.cw ? 2 * c.cw : 1;
+  if (n_items > 0) {
+    shard_requests<<<grid_for(n_items, 256), 256, 0, st>>>(c.bw.half[0].idx, item_begin, n_items, c.R, ctxw,
+                                                           vocab_global, nshard, 0, cursor, keys, items, ident);
+    WV_LAUNCH_CHECK();
+  }
+  shard_offsets<<<1, 1, 0, st>>>(cursor, nshard, counts);
+  WV_LAUNCH_CHECK();
+  if (n_items > 0) {
+    shard_requests<<<grid_for(n_items, 256), 256, 0, st>>>(c.bw.half[0].idx, item_begin, n_items, c.R, ctxw,
+                                                           vocab_global, nshard, 1, cursor, keys, items, ident);
+    WV_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+int wv_shard_serve(const WvSgnsModel* model, const int64_t* keys, int64_t n, int64_t vocab_global, int nshard,
+                   void* rows, void* stream) {
+  using namespace wv;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = model->vector_size;
+  if (model->precision == WV_FP32)
+    shard_serve<float><<<grid_for(n * d, 256), 256, 0, st>>>((const float*)model->input, (const float*)model->output,
+                                                             keys, n, vocab_global, nshard, d, (float*)rows);
+  else
+    shard_serve<double><<<grid_for(n * d, 256), 256, 0, st>>>((const double*)model->input,
+                                                              (const double*)model->output, keys, n, vocab_global,
+                                                              nshard, d, (double*)rows);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int wv_shard_place(const void* rows, const int32_t* items, int64_t n, int vector_size, int precision,
+                   void* itemrows, void* stream) {
+  using namespace wv;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = vector_size;
+  if (precision == WV_FP32)
+    shard_place<float><<<grid_for(n * d, 256), 256, 0, st>>>((const float*)rows, items, n, d, (float*)itemrows);
+  else
+    shard_place<double><<<grid_for(n * d, 256), 256, 0, st>>>((const double*)rows, items, n, d, (double*)itemrows);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+// the rank's pairs [pair_begin, pair_begin + pair_count) of the global batch:
+// rows from itemrows (item order, ident = item index or -1), U/G/coef out in
+// local pair order; gradients normalised by the global batch's rows
+int wv_shard_gather(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                    int64_t vocab_global, int nshard, int shard, const void* itemrows, const int32_t* ident,
+                    int64_t pair_count, void* U, void* G, void* coef, void* stream) {
+  using namespace wv;
+  BatchCtx c;
+  WV_CUDA_RC(shard_ctx(model, batch, ws, ws_bytes, vocab_global, nshard, shard, c));
+  if (pair_count == 0) return 0;
+  PairArgs pa = pair_args(c, 0);
+  pa.Bn = c.B;
+  pa.B = pair_count;
+  pa.idx = const_cast<int32_t*>(ident);
+  pa.U = U;
+  pa.G = G;
+  pa.coef = coef;
+  const unsigned pgrid = grid_for(pair_count, kPairWarps, 148 * 32);
+  return dispatch_rows<LaunchPair>(model->precision, c.d, pa, itemrows, itemrows, pgrid, (cudaStream_t)stream);
+}
+
+// slot-ordered sums + RowAdam on the rank's rows, U/G/coef in global-batch order
+int wv_shard_update(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws, int64_t ws_bytes,
+                    int64_t vocab_global, int nshard, int shard, const void* U, const void* G, const void* coef,
+                    void* stream) {
+  using namespace wv;
+  BatchCtx c;
+  WV_CUDA_RC(shard_ctx(model, batch, ws, ws_bytes, vocab_global, nshard, shard, c));
+  c.bw.U = const_cast<void*>(U);
+  c.bw.G = const_cast<void*>(G);
+  c.bw.coef = const_cast<void*>(coef);
+  SideStream* ss = nullptr;
+  WV_CUDA(side_stream(&ss));
+  return enqueue_update(c, 0, ss, (cudaStream_t)stream);
+}
+
 #undef WV_STAMP
 
 }  // extern "C"

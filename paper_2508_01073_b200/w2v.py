@@ -181,9 +181,15 @@ class EmbeddingModel:
 class _Params:
     """Device parameter store + optimizer state of one replica."""
 
-    def __init__(self, torch, dev, V: int, d: int, seed: int, precision: str, sparse: bool, lr: float):
+    def __init__(self, torch, dev, V: int, d: int, seed: int, precision: str, sparse: bool, lr: float,
+                 shard: tuple[int, int] | None = None):
+        """``shard=(nshard, rank)``: hold only the rows r with r % nshard == rank (row-sharded mode)."""
         self.torch = torch
         self.dev = dev
+        self.V_global = int(V)
+        self.shard = shard
+        if shard is not None:
+            V = -(-int(V) // shard[0])
         self.V, self.d = int(V), int(d)
         self.seed = int(seed)
         self.precision = _lib.FP64 if precision == "fp64" else _lib.FP32
@@ -216,8 +222,12 @@ class _Params:
         self.state = host.to(dev)
         words, nw = words_array(entropy_words([seed, 1, 0]))
         self._init_words = (words, nw)
-        _lib.call("wv_sgns_init", self.V, self.d, words, nw, self.precision, _lib.ptr(self.inp), _lib.ptr(self.out),
-                  _lib.stream_ptr())
+        if shard is None:
+            _lib.call("wv_sgns_init", self.V, self.d, words, nw, self.precision, _lib.ptr(self.inp),
+                      _lib.ptr(self.out), _lib.stream_ptr())
+        else:
+            _lib.call("wv_shard_init", self.V_global, self.d, words, nw, self.precision, int(shard[0]),
+                      int(shard[1]), _lib.ptr(self.inp), _lib.ptr(self.out), _lib.stream_ptr())
         self.struct = _lib.WvSgnsModel(
             vocab_size=self.V, vector_size=self.d, precision=self.precision, sparse=int(self.sparse), pad=0,
             learning_rate=self.lr, input=_lib.ptr(self.inp), output=_lib.ptr(self.out), m_in=_lib.ptr(self.m_in),
