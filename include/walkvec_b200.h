@@ -283,6 +283,28 @@ int wv_replica_delta(const void* params, const void* snapshot, int64_t n, int pr
 int wv_replica_apply(void* params, void* snapshot, const void* delta_sum, const float* touch_count, int64_t rows,
                      int vector_size, int precision, void* stream);
 
+/* --------------------------------------------------------------- ingest --
+ * GPU ingest: ingest.parse_ntriples / parse_edge_table +
+ * build_vocabulary (ingest.py:116-257, 368-396) over raw UTF-8 file bytes.
+ * Phase 1 finds universal-newline line terminators (line_end[n_terms]);
+ * phase 2 parses every line (mode 0 N-Triples, 1 whitespace table, 2
+ * `delim`-separated table), interns keys by first occurrence (64-bit hash of
+ * the unescaped key, every occurrence verified against its first one) and
+ * writes edges, roles and each token's key span.  n_lines = n_terms, + 1
+ * when the text does not end with a terminator (the caller then sets
+ * line_end[n_terms] = n_bytes).  Per line status: 0 skipped,
+ * 1 statement, 2 ParseError, 3 ValueError; err = code (negative: -columns),
+ * err_at = byte position; bad[2] = first error line, first ValueError line;
+ * n_out = {statements, edges, vocabulary size, hash-collision flag}. */
+int64_t wv_ingest_lines_workspace_bytes(int64_t n_bytes);
+int wv_ingest_lines(const uint8_t* text, int64_t n_bytes, int64_t* line_end, int64_t* n_terms, void* ws,
+                    int64_t ws_bytes, void* stream);
+int64_t wv_ingest_workspace_bytes(int64_t n_lines);
+int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_end, int64_t n_lines, int mode,
+                    int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
+                    int64_t* bad, int64_t* n_out, int64_t* edges, uint32_t* roles, int64_t* tok_span, void* ws,
+                    int64_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ synthetic --
  * Measurement inputs (BASELINE.json configs).  gen_barabasi restates
  * benchgen.gen_barabasi (benchgen.py:78-109): vertex v >= 1 adds min(m, v)

@@ -14,9 +14,10 @@ backend (random_walks, bfs_walks, train, build_graph, extract_walks).
 
 from ._lib import BackendUnavailable
 from .graph import Graph, build_graph
-from .ingest import PAD, Vocabulary, build_vocabulary, encode_integer_triples
+from .ingest import PAD, ParseError, Vocabulary, build_vocabulary, encode_integer_triples, load_triples_device
 from .install import install, uninstall
-from .pipeline import EmbeddingTable, PipelineConfig, PipelineError, extract_walks, fit_transform
+from .pipeline import (EmbeddingTable, PipelineConfig, PipelineError, detect_format, extract_walks, fit_transform,
+                       load_data)
 from .w2v import (
     CBOW,
     SKIPGRAM,
@@ -55,7 +56,7 @@ __all__ = [
     "BFS", "CBOW", "ENTITY", "FULL", "PAD", "PROPERTY", "RANDOM", "SHARD_SIZE", "SKIPGRAM",
     "BackendUnavailable", "EmbeddingModel", "EmbeddingTable", "Graph", "PathTable", "PipelineConfig",
     "PipelineError", "SkipGramSession", "TrainConfig", "TrainingDiverged", "Vocabulary", "Walk", "WalkCorpus",
-    "bfs_walks", "build_graph", "build_vocabulary", "encode_integer_triples", "estimate_per_sample_bytes",
+    "ParseError", "bfs_walks", "build_graph", "build_vocabulary", "detect_format", "load_data", "load_triples_device", "encode_integer_triples", "estimate_per_sample_bytes",
     "extract_walks", "fit_transform", "generate_cbow_instances", "generate_pairs", "init_embeddings", "install", "project_corpus",
     "project_entity", "project_property", "random_walks", "resolve_memory_budget", "suggest_batch_size",
     "train", "uninstall",

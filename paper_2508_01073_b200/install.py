@@ -5,7 +5,8 @@ hot path through module attributes -- pipeline.extract_walks ->
 walks_mod.random_walks / bfs_walks (pipeline.py:20, 167, 178), and
 ``train`` imported by name into pipeline (pipeline.py:23, 211), cli
 (cli.py:21, 169) and re-exported from the package.  install() swaps exactly
-those attributes; uninstall() restores them.
+those attributes, plus ``load_data`` (pipeline.py:117, cli.py:103; GPU ingest);
+uninstall() restores them.
 """
 
 from __future__ import annotations
@@ -26,9 +27,33 @@ def _wrap_train(train_fn):
     return train
 
 
+def _wrap_load_data(load_fn, pkg_name: str):
+    """Device ingest, returning the reference's own Vocabulary type (save_tsv etc.)."""
+
+    def load_data(path, format=None, include_literals=False, strict=False, has_header=False, error_sink=None):
+        ref_ingest = importlib.import_module(f"{pkg_name}.ingest")
+        ref_pipe = importlib.import_module(f"{pkg_name}.pipeline")
+        from .pipeline import PipelineError
+
+        try:
+            vocab, edges = load_fn(path, format=format, include_literals=include_literals, strict=strict,
+                                   has_header=has_header, error_sink=error_sink)
+        except PipelineError as err:
+            raise ref_pipe.PipelineError("ingest", err.__cause__ or err) from err
+        ref = ref_ingest.Vocabulary()
+        ref.lexical_of = list(vocab.lexical_of)
+        ref.token_of = {s_: i for i, s_ in enumerate(ref.lexical_of)}
+        ref._entity_tokens = set(vocab.entity_tokens().tolist())
+        ref._predicate_tokens = set(vocab._predicate_tokens)
+        return ref, edges
+
+    return load_data
+
+
 def install(package: str = "walkvec"):
     """Swap the reference's hot-path functions for the device implementations."""
     from . import walks as dev_walks
+    from .pipeline import load_data as dev_load_data
     from .w2v import train as dev_train
 
     pkg = importlib.import_module(package)
@@ -43,6 +68,8 @@ def install(package: str = "walkvec"):
         (w2v_mod, "train", _wrap_train(dev_train)),
         (pipe_mod, "train", _wrap_train(dev_train)),
         (pkg, "train", _wrap_train(dev_train)),
+        (pipe_mod, "load_data", _wrap_load_data(dev_load_data, package)),
+        (pkg, "load_data", _wrap_load_data(dev_load_data, package)),
     ]
     try:
         cli_mod = importlib.import_module(f"{package}.cli")

@@ -114,6 +114,47 @@ class EmbeddingTable:
         return {lex: self.vectors[tok] for lex, tok in self.vocab.token_of.items()}
 
 
+_FORMATS = ("nt", "csv", "tsv", "txt")
+_UNSUPPORTED = {".parquet": "parquet", ".orc": "orc"}
+
+
+def detect_format(path) -> str:
+    """File format from the extension (pipeline.py:107-114)."""
+    from pathlib import Path
+
+    suffix = Path(path).suffix.lower()
+    if suffix in _UNSUPPORTED:
+        raise ValueError(f"format unsupported: {_UNSUPPORTED[suffix]}")
+    mapped = {".nt": "nt", ".csv": "csv", ".tsv": "tsv", ".txt": "txt"}.get(suffix)
+    if mapped is None:
+        raise ValueError(f"cannot infer format from {suffix!r}; pass format explicitly")
+    return mapped
+
+
+def load_data(path, format: str | None = None, include_literals: bool = False, strict: bool = False,
+              has_header: bool = False, error_sink: list | None = None):
+    """Parse and tokenize an input file on the GPU: (vocabulary, edges) (pipeline.py:117-135).
+
+    The file's bytes go to the device once; lines are parsed and keys interned
+    by first occurrence there (``ingest.load_triples_device``).  Errors are the
+    reference's: ValueError for formats, ParseError / ValueError from parsing,
+    wrapped as ``PipelineError("ingest", ...)``.
+    """
+    from .ingest import load_triples_device
+
+    if format is None:
+        format = detect_format(path)
+    if format not in _FORMATS:
+        if format in _UNSUPPORTED.values():
+            raise ValueError(f"format unsupported: {format}")
+        raise ValueError(f"unknown format: {format!r}")
+    try:
+        return load_triples_device(path, format, strict=strict, error_sink=error_sink,
+                                   include_literals=include_literals, has_header=has_header)
+    except (ValueError, OSError) as err:
+        raise PipelineError("ingest", err) from err
+
+
 def extract_walks(graph, roots, config: PipelineConfig, *, rng: str = "pcg64",
                   max_walks_per_root: int | None = None) -> WalkCorpus:
     """Configured walk strategy + projection (pipeline.py:164-179)."""

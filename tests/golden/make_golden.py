@@ -8,6 +8,7 @@ tests read only these committed files.
 
 from __future__ import annotations
 
+import io
 import json
 import sys
 from pathlib import Path
@@ -202,6 +203,101 @@ def cbow():
     np.savez_compressed(OUT / "cbow.npz", **out)
 
 
+def ingest_cases():
+    """N-Triples and edge-table inputs through the reference's parse + build_vocabulary
+    (ingest.py:116-257, 368-396): tokens, lexicals, roles, edges and errors."""
+    import tempfile
+
+    from walkvec.ingest import ParseError, parse_edge_table, parse_ntriples
+
+    good = (
+        '<http://x/a> <http://x/p> <http://x/b> .\n'
+        '# a comment line\n'
+        '\n'
+        '_:b1 <http://x/p> "lit \\"q\\" \\u00e9" .\r\n'
+        '<http://x/b>\t<http://x/q> "12"^^<http://www.w3.org/2001/XMLSchema#int> . # tail comment\r'
+        '<http://x/\\u0063> <http://x/p> "hello"@en-GB .\n'
+        '<http://x/p> <http://x/q> <http://x/c> .\n'
+        '  <http://x/c> <http://x/p> _:b1 .\n'
+        '<http://x/é> <http://x/p> <http://x/a> .\n'
+        '<_:b1> <http://x/q> "x\\ty" .'
+    )
+    bad_lines = [
+        '<http://x/a> <http://x/p> <http://x/b>',
+        '<http://x/a <http://x/p> <http://x/b> .',
+        '_: <http://x/p> <http://x/b> .',
+        '<http://x/a> <http://x/p> "open .',
+        '<http://x/a> <http://x/p> "v"^^http://t .',
+        '<http://x/a> <http://x/p> "v"^^<http://t .',
+        '<http://x/a> <http://x/p> "v"@ .',
+        '<http://x/a> <http://x/p> ?x .',
+        '"s" <http://x/p> <http://x/b> .',
+        '<http://x/a> _:p <http://x/b> .',
+        '<http://x/a> <http://x/p> <http://x/b> . junk',
+        '<http://x/a> <http://x/p> "bad \\q" .',
+        '<http://x/a> <http://x/p> "bad \\u12" .',
+        '<http://x/a> <http://x/p> "bad \\uZZZZ" .',
+        '<http://x/a> <http://x/p> "bad \\U00110000" .',
+        '<http://x/a> <http://x/p>',
+    ]
+    cases = []
+    for include in (False, True):
+        vocab, edges = build_vocabulary(parse_ntriples(io.BytesIO(good.encode())), include_literals=include)
+        cases.append(dict(name=f"good_lit{int(include)}", format="nt", text=good, include_literals=include,
+                          strict=False, lexicals=vocab.lexical_of, edges=edges.tolist(),
+                          entities=vocab.entity_tokens().tolist(), predicates=sorted(vocab._predicate_tokens)))
+    mixed = "\n".join(["<http://x/a> <http://x/p> <http://x/b> ."] + bad_lines + ["<http://x/b> <http://x/p> <http://x/z> ."])
+    sink = []
+    vocab, edges = build_vocabulary(parse_ntriples(io.BytesIO(mixed.encode()), error_sink=sink))
+    cases.append(dict(name="mixed_nonstrict", format="nt", text=mixed, include_literals=False, strict=False,
+                      lexicals=vocab.lexical_of, edges=edges.tolist(), entities=vocab.entity_tokens().tolist(),
+                      predicates=sorted(vocab._predicate_tokens),
+                      errors=[[e.line, e.reason] for e in sink]))
+    for i, line in enumerate(bad_lines):
+        text = "<http://x/a> <http://x/p> <http://x/b> .\n" + line + "\n"
+        try:
+            build_vocabulary(parse_ntriples(io.BytesIO(text.encode()), strict=True))
+            raise AssertionError("expected a ParseError")
+        except ParseError as e:
+            cases.append(dict(name=f"strict_{i}", format="nt", text=text, strict=True, include_literals=False,
+                              error=[e.line, e.reason]))
+    try:
+        build_vocabulary(parse_ntriples(io.BytesIO(b"<> <http://x/p> <http://x/b> .\n")))
+    except ValueError as e:
+        cases.append(dict(name="value_error", format="nt", text="<> <http://x/p> <http://x/b> .\n", strict=False,
+                          include_literals=False, value_error=str(e)))
+    tables = {
+        "csv": "s,p,o\na,r,b\nb,r,c\n\nc,q,a\r\na,q,c",
+        "tsv": "a\tr\tb\nb\tq\tc\n",
+        "txt": "a r b\n\n  b  q\tc \nc r a\n",
+    }
+    for fmt, text in tables.items():
+        for header in (False, True):
+            with tempfile.NamedTemporaryFile("w", suffix="." + fmt, delete=False, newline="") as fh:
+                fh.write(text)
+            vocab, edges = build_vocabulary(parse_edge_table(fh.name, format=fmt, has_header=header))
+            cases.append(dict(name=f"table_{fmt}_{int(header)}", format=fmt, text=text, has_header=header,
+                              strict=False, include_literals=False, lexicals=vocab.lexical_of, edges=edges.tolist(),
+                              entities=vocab.entity_tokens().tolist(), predicates=sorted(vocab._predicate_tokens)))
+    with tempfile.NamedTemporaryFile("w", suffix=".csv", delete=False, newline="") as fh:
+        fh.write("a,r,b\nb,r\n")
+    try:
+        build_vocabulary(parse_edge_table(fh.name, format="csv"))
+    except ParseError as e:
+        cases.append(dict(name="table_columns", format="csv", text="a,r,b\nb,r\n", strict=False,
+                          include_literals=False, error=[e.line, e.reason]))
+    rows = [("a b", "p>q", "c\\d", "resource"), ("_:b1", "p>q", 'say "hi"\nnow', "literal"),
+            ("c\\d", "r", "a b", "resource"), ("é", "p>q", "_:b1", "resource"), ("x", "r", "é", "literal"),
+            ("<y>", "r", "x", "resource")]
+    for include in (False, True):
+        vocab, edges = build_vocabulary([Triple(s_, p_, o_, k_) for s_, p_, o_, k_ in rows],
+                                        include_literals=include)
+        cases.append(dict(name=f"triples_lit{int(include)}", triples=rows, include_literals=include,
+                          lexicals=vocab.lexical_of, edges=edges.tolist(), entities=vocab.entity_tokens().tolist(),
+                          predicates=sorted(vocab._predicate_tokens)))
+    (OUT / "ingest.json").write_text(json.dumps(cases, indent=1, ensure_ascii=False) + "\n")
+
+
 def two_clique():
     rows = []
     for base in ("x", "y"):
@@ -243,7 +339,8 @@ def vocab_encoding():
 
 if __name__ == "__main__":
     # python make_golden.py [generator ...]   (default: all)
-    gens = {f.__name__: f for f in (seedseq, walks, bfs, embeddings_and_train, two_clique, vocab_encoding, cbow)}
+    gens = {f.__name__: f for f in (seedseq, walks, bfs, embeddings_and_train, two_clique, vocab_encoding, cbow,
+                                    ingest_cases)}
     for name in (sys.argv[1:] or list(gens)):
         gens[name]()
     for p in sorted(OUT.glob("*.np*")) + sorted(OUT.glob("*.json")):
