@@ -196,6 +196,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             raise BackendUnavailable(f"{LIB_PATH} is missing; run paper_2508_01073_b200/_build.py")
         lib = C.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("WV_LIB") and not hasattr(lib, name):
+                continue  # A/B builds of older revisions: bind what they export
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

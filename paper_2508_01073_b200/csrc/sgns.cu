@@ -258,10 +258,6 @@ struct PairArgs {
   int R;   // rows per item: 2 + k (skip-gram) or 2W + 1 + k (CBOW)
   int cw;  // CBOW window W (0: skip-gram)
   int64_t B;  // rows in this batch
-  int64_t Bn;     // gradient normaliser (rows of the global batch; 0: B)
-  int nshard;     // row-sharded mode: this rank claims rows r with r % nshard == shard
-  int shard;
-  int64_t Vl;     // local rows per matrix (key space of the claims: [0, 2 Vl))
   const CorpusDesc* desc;
   // outputs
   void* U;
@@ -273,6 +269,10 @@ struct PairArgs {
   int32_t* idx;    // [B, 2+k] centre, context, negatives
   double* partials;
   WvSgnsDevState* state;
+  int64_t Bn;     // gradient normaliser (rows of the global batch; 0: B)
+  int nshard;     // row-sharded mode: this rank claims rows r with r % nshard == shard
+  int shard;
+  int64_t Vl;     // local rows per matrix (key space of the claims: [0, 2 Vl))
 };
 
 // ------------------------------------------------------------ grouping ---
@@ -305,8 +305,10 @@ __device__ __forceinline__ bool owned_key(uint32_t key, int64_t V, int nshard, i
 }
 
 __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
-  uint32_t lk;
-  if (!owned_key(key, A.V, A.nshard, A.shard, A.Vl, lk)) return;
+  uint32_t lk = key;
+#ifndef WV_NO_SHARD_CLAIM
+  if (A.nshard > 1 && !owned_key(key, A.V, A.nshard, A.shard, A.Vl, lk)) return;
+#endif
   if (atomicAdd(A.cnt + lk, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = lk;
 }
 
@@ -333,20 +335,22 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
   if (threadIdx.x == 0) D = *A.desc;
   __syncthreads();
   const int k = A.k;
-  const int R = A.R;
+  const int R = 2 + k;
   const int64_t B = A.B;
-  const int64_t items = B * R;
+  // work items: [0, B) decode pair b (centre + context); [B, B + Bk) draw
+  // negative j of pair b.  The two kinds never share a warp except at the one
+  // boundary, so the long pair-decode chains do not hold the negatives' lanes.
+  const int64_t items = B * (1 + k);
   const int64_t lo = A.state->lo;
   const uint64_t epoch = (uint64_t)A.state->epoch;
   Feistel fs;
   if (D.mode == WV_PAIRS_NATIVE) fs = make_feistel(D.seed, epoch, D.N);
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
        it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = it / R;
-    const int jj = (int)(it - b * R);
-    const int64_t pos = lo + b;
-    int32_t* row = A.idx + b * R;
-    if (jj == 0) {
+    if (it < B) {
+      const int64_t b = it;
+      const int64_t pos = lo + b;
+      int32_t* row = A.idx + b * R;
       int32_t center, context;
       if (D.mode == WV_PAIRS_NATIVE) {
         const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, D.N);
@@ -375,8 +379,11 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       row[1] = context;
       group_claim(A, (uint32_t)center);
       group_claim(A, (uint32_t)(context + A.V));
-    } else if (jj >= 2) {
-      const int j = jj - 2;
+    } else {
+      const int64_t t = it - B;
+      const int64_t b = t / k;
+      const int j = (int)(t - b * k);
+      const int64_t pos = lo + b;
       int32_t neg;
       if (D.mode == WV_PAIRS_NATIVE) {
         // Philox4x32 counter (position, epoch, j/2): two draws per call
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       } else {
         neg = D.negatives[pos * k + j];
       }
-      row[jj] = neg;
+      A.idx[b * R + 2 + j] = neg;
       group_claim(A, (uint32_t)(neg + A.V));
     }
   }
@@ -1582,6 +1589,9 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
 #ifndef WV_PIECE_GRID
 #define WV_PIECE_GRID 148
 #endif
+#ifndef WV_FLAT_PREFETCH
+#define WV_FLAT_PREFETCH 0
+#endif
 constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
 template <typename T, int EPC, int MAXC>
 __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc);
@@ -1611,6 +1621,35 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
   const uint32_t total = nseg * C;
   const uint32_t stride = gridDim.x * blockDim.x * kFlatU;
   for (uint32_t i0 = blockIdx.x * blockDim.x * kFlatU + threadIdx.x; i0 < total; i0 += stride) {
+    if (WV_FLAT_PREFETCH > 0) {
+      // L2 prefetch of the optimizer-state rows this thread's item will touch
+      // WV_FLAT_PREFETCH iterations ahead (one bulk prefetch per row and array,
+      // issued by the thread holding the row's chunk 0 or the warp's first lane)
+      const uint32_t i2 = i0 + (uint32_t)WV_FLAT_PREFETCH * stride;
+      if (i2 < total) {
+        uint32_t r2 = __umulhi(i2, A.cmag);
+        int32_t c2 = (int32_t)(i2 - r2 * C);
+        if (c2 < 0) {
+          --r2;
+          c2 += (int32_t)C;
+        } else if (c2 >= (int32_t)C) {
+          ++r2;
+          c2 -= (int32_t)C;
+        }
+        if (c2 == 0 || (threadIdx.x & 31) == 0) {
+          const uint32_t key = A.segs[r2].key;
+          const bool so = key >= (uint32_t)A.V;
+          const int64_t row = so ? (int64_t)key - A.V : (int64_t)key;
+          const uint32_t bytes = (uint32_t)(d * sizeof(T));
+          const T* rows3[3] = {(const T*)(so ? A.out : A.in), (const T*)(so ? A.m_out : A.m_in),
+                               (const T*)(so ? A.v_out : A.v_in)};
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rows3[a] + row * d), "r"(bytes)
+                         : "memory");
+        }
+      }
+    }
     Segment sg[kFlatU];
     int32_t cr[kFlatU];
     bool ok[kFlatU];
