@@ -273,6 +273,7 @@ struct PairArgs {
   int nshard;     // row-sharded mode: this rank claims rows r with r % nshard == shard
   int shard;
   int64_t Vl;     // local rows per matrix (key space of the claims: [0, 2 Vl))
+  uint32_t* rank; // [items] an item's position among its row's items (from the claim)
 };
 
 // ------------------------------------------------------------ grouping ---
@@ -304,12 +305,14 @@ __device__ __forceinline__ bool owned_key(uint32_t key, int64_t V, int nshard, i
   return true;
 }
 
-__device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key) {
+// count the item on its row (the returned count is the item's rank in the
+// row's list, so placement needs no second atomic); the first claims the row
+__device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key, int64_t item) {
   uint32_t lk = key;
-#ifndef WV_NO_SHARD_CLAIM
   if (A.nshard > 1 && !owned_key(key, A.V, A.nshard, A.shard, A.Vl, lk)) return;
-#endif
-  if (atomicAdd(A.cnt + lk, 1u) == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = lk;
+  const uint32_t r = atomicAdd(A.cnt + lk, 1u);
+  A.rank[item] = r;
+  if (r == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = lk;
 }
 
 // Phase 1a, thread per item: the batch's row indices (centre, context, k
@@ -377,8 +380,8 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       }
       row[0] = center;
       row[1] = context;
-      group_claim(A, (uint32_t)center);
-      group_claim(A, (uint32_t)(context + A.V));
+      group_claim(A, (uint32_t)center, b * R);
+      group_claim(A, (uint32_t)(context + A.V), b * R + 1);
     } else {
       const int64_t t = it - B;
       const int64_t b = t / k;
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
         neg = D.negatives[pos * k + j];
       }
       A.idx[b * R + 2 + j] = neg;
-      group_claim(A, (uint32_t)(neg + A.V));
+      group_claim(A, (uint32_t)(neg + A.V), b * R + 2 + j);
     }
   }
 }
@@ -426,11 +429,11 @@ __global__ void __launch_bounds__(128) cbow_decode_kernel(PairArgs A) {
       const int64_t q = D.mode == WV_PAIRS_NATIVE ? (int64_t)feistel_perm(fs, (uint64_t)pos, D.N) : D.perm[pos];
       const int32_t t = D.inst[q * (ctxw + 1) + jj];
       row[jj] = t;
-      if (t >= 0) group_claim(A, (uint32_t)t + (jj == ctxw ? (uint32_t)A.V : 0u));
+      if (t >= 0) group_claim(A, (uint32_t)t + (jj == ctxw ? (uint32_t)A.V : 0u), it);
     } else {
       const int32_t neg = draw_negative(D, pos, epoch, jj - ctxw - 1, k);
       row[jj] = neg;
-      group_claim(A, (uint32_t)(neg + A.V));
+      group_claim(A, (uint32_t)(neg + A.V), it);
     }
   }
 }
@@ -941,25 +944,42 @@ __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __re
     const bool ok = u < nu;
     const uint32_t key = ok ? uniq[u] : 0u;
     const uint32_t len = ok ? cnt[key] : 0u;
-    // warp-aggregated list reservation
+    // block-aggregated reservations: one atomic per block and counter (the
+    // three counters are single addresses every block contends on)
     uint32_t incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += n;
     }
-    uint32_t wbase = 0;
-    if (lane == 31) wbase = atomicAdd(gctr + GC_TOTAL, incl);
-    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-    const uint32_t start = wbase + incl - len;
     const bool is_heavy = ok && len > (uint32_t)kLightMax;
     const uint32_t ml = __ballot_sync(0xffffffffu, ok && !is_heavy);
     const uint32_t mh = __ballot_sync(0xffffffffu, is_heavy);
-    uint32_t lb = 0, hb = 0;
-    if (lane == 0 && ml) lb = atomicAdd(gctr + GC_LIGHT, (uint32_t)__popc(ml));
-    if (lane == 0 && mh) hb = atomicAdd(gctr + GC_HEAVY, (uint32_t)__popc(mh));
-    lb = __shfl_sync(0xffffffffu, lb, 0);
-    hb = __shfl_sync(0xffffffffu, hb, 0);
+    __shared__ uint32_t wsum[3][32];
+    __shared__ uint32_t bbase[3];
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (lane == 31) {
+      wsum[0][warp] = incl;
+      wsum[1][warp] = __popc(ml);
+      wsum[2][warp] = __popc(mh);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      uint32_t run = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const uint32_t v = wsum[threadIdx.x][w];
+        wsum[threadIdx.x][w] = run;
+        run += v;
+      }
+      bbase[threadIdx.x] = run ? atomicAdd(gctr + (threadIdx.x == 0 ? GC_TOTAL : threadIdx.x == 1 ? GC_LIGHT
+                                                                                                   : GC_HEAVY), run)
+                               : 0u;
+    }
+    __syncthreads();
+    const uint32_t start = bbase[0] + wsum[0][warp] + incl - len;
+    const uint32_t lb = bbase[1] + wsum[1][warp];
+    const uint32_t hb = bbase[2] + wsum[2][warp];
+    __syncthreads();  // wsum / bbase are rewritten by the next iteration
     if (ok) {
       cnt[key] = start;  // becomes the placement cursor
       Segment sg;
@@ -1055,6 +1075,35 @@ __global__ void group_place_agg(const int32_t* __restrict__ idx, int64_t B, int 
     if (lane == leader && key != 0xffffffffu) pos = atomicAdd(cnt + key, (uint32_t)__popc(peers));
     pos = __shfl_sync(0xffffffffu, pos, leader);
     if (key != 0xffffffffu) list[pos + rank] = slot;
+  }
+}
+
+// every claimed item writes its slot at (row's list start + its claim rank):
+// no atomics (group_segments turned cnt[key] into the list start)
+__global__ void group_place_rank(const int32_t* __restrict__ idx, const uint32_t* __restrict__ rank, int64_t B, int k,
+                                 int R, int cw, int64_t V, const uint32_t* __restrict__ cnt,
+                                 uint32_t* __restrict__ list, int nshard, int shard, int64_t Vl) {
+  const int64_t items = B * R;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < items; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / R;
+    const int j = (int)(i - b * R);
+    const int32_t t = idx[i];
+    uint32_t key, slot;
+    if (cw == 0) {
+      key = (uint32_t)t + (j == 0 ? 0u : (uint32_t)V);
+      slot = (uint32_t)(j == 0 ? b : (j == 1 ? B + b : 2 * B + b * k + (j - 2)));
+    } else {
+      if (t < 0) continue;
+      const int ctxw = 2 * cw;
+      key = (uint32_t)t + (j < ctxw ? 0u : (uint32_t)V);
+      slot = (uint32_t)(j < ctxw ? b * ctxw + j : (j == ctxw ? b : B + b * k + (j - ctxw - 1)));
+    }
+    if (nshard > 1) {
+      uint32_t lk;
+      if (!owned_key(key, V, nshard, shard, Vl, lk)) continue;
+      key = lk;
+    }
+    list[cnt[key] + rank[i]] = slot;
   }
 }
 
@@ -2648,6 +2697,7 @@ struct BatchHalf {
   uint2* pieces;     // heavy-row pieces (row, piece index)
   void* partial;     // [max_pieces, d] piece partial sums
   uint32_t* rowdone; // per heavy row: pieces finished (zero between batches)
+  uint32_t* rank;    // [items] claim rank of each item within its row
 };
 
 struct BatchWs {
@@ -2695,6 +2745,7 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int R, int64_
     x.pieces = (uint2*)take(max_pieces(items) * 8);
     x.partial = take(max_pieces(items) * d * es);
     x.rowdone = (uint32_t*)take((items / (kLightMax + 1) + 1) * 4);  // zeroed per batch with gctr
+    x.rank = (uint32_t*)take(items * 4);
   }
   return off + 1024;
 }
@@ -3119,6 +3170,7 @@ static PairArgs pair_args(const BatchCtx& c, int h) {
   pa.uniq = c.bw.half[h].uniq;
   pa.gctr = c.bw.half[h].gctr;
   pa.idx = c.bw.half[h].idx;
+  pa.rank = c.bw.half[h].rank;
   pa.partials = c.bw.partials;
   pa.state = c.model->state;
   return pa;
@@ -3205,8 +3257,8 @@ static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
                                                                   m->steps_out, x.segs, x.heavy, c.items, m->state,
                                                                   c.B, bct);
   WV_LAUNCH_CHECK();
-  group_place_agg<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, c.B, c.k, c.R, c.cw, c.Vtok, x.cnt, x.list,
-                                                                   c.nshard, c.shard, c.V);
+  group_place_rank<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, x.rank, c.B, c.k, c.R, c.cw, c.Vtok,
+                                                                    x.cnt, x.list, c.nshard, c.shard, c.V);
   WV_LAUNCH_CHECK();
   if (flat_owner(c)) {
     group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, c.sm);
