@@ -308,11 +308,24 @@ __device__ __forceinline__ bool owned_key(uint32_t key, int64_t V, int nshard, i
 // count the item on its row (the returned count is the item's rank in the
 // row's list, so placement needs no second atomic); the first claims the row
 __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key, int64_t item) {
+  const uint32_t active = __activemask();
   uint32_t lk = key;
-  if (A.nshard > 1 && !owned_key(key, A.V, A.nshard, A.shard, A.Vl, lk)) return;
-  const uint32_t r = atomicAdd(A.cnt + lk, 1u);
-  A.rank[item] = r;
-  if (r == 0u) A.uniq[atomicAdd(A.gctr + GC_UNIQUE, 1u)] = lk;
+  const bool owned = A.nshard <= 1 || owned_key(key, A.V, A.nshard, A.shard, A.Vl, lk);
+  bool first = false;
+  if (owned) {
+    const uint32_t r = atomicAdd(A.cnt + lk, 1u);
+    A.rank[item] = r;
+    first = r == 0u;
+  }
+  // new rows take unique ids with one atomic per warp (GC_UNIQUE is one address)
+  const uint32_t fm = __ballot_sync(active, first);
+  if (fm == 0u) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(fm) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(A.gctr + GC_UNIQUE, (uint32_t)__popc(fm));
+  base = __shfl_sync(active, base, leader);
+  if (first) A.uniq[base + __popc(fm & ((1u << lane) - 1u))] = lk;
 }
 
 // Phase 1a, thread per item: the batch's row indices (centre, context, k
