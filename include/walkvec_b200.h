@@ -305,6 +305,21 @@ int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_en
                     int64_t* bad, int64_t* n_out, int64_t* edges, uint32_t* roles, int64_t* tok_span, void* ws,
                     int64_t ws_bytes, void* stream);
 
+/* -------------------------------------------------------------- formats --
+ * Writers of SURVEY §8f row 3, formatted on the device.  Text export of `rows`
+ * vectors (fp32 / fp64 [rows, d]) as "<lexical><sep>%.8g<sep>...\n" lines
+ * (pipeline.save_embeddings_text / _tsv, pipeline.py:236-251; Python's
+ * correctly rounded %.8g): plan -> *total bytes (device int64), *bad = 1 if a
+ * value is outside [1e-30, 1e16) in magnitude (and not 0, inf or nan); emit ->
+ * the bytes.  WVC1 corpus body (walks.save_corpus_binary, walks.py:344-364):
+ * per walk a u32 length then its u32 tokens (header written by the caller). */
+int64_t wv_format_workspace_bytes(int64_t rows, int d);
+int wv_format_plan(const void* vec, int precision, int64_t rows, int d, const int64_t* lex_off, int64_t* total,
+                   int* bad, void* ws, int64_t ws_bytes, void* stream);
+int wv_format_emit(const char* lex, const int64_t* lex_off, int64_t rows, int d, char sep, char* out, void* ws,
+                   int64_t ws_bytes, void* stream);
+int wv_wvc1_pack(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, uint32_t* body, void* stream);
+
 /* ------------------------------------------------------------ synthetic --
  * Measurement inputs (BASELINE.json configs).  gen_barabasi restates
  * benchgen.gen_barabasi (benchgen.py:78-109): vertex v >= 1 adds min(m, v)

@@ -13,6 +13,7 @@ backend (random_walks, bfs_walks, train, build_graph, extract_walks).
 """
 
 from ._lib import BackendUnavailable
+from . import formats
 from .graph import Graph, build_graph
 from .ingest import PAD, ParseError, Vocabulary, build_vocabulary, encode_integer_triples, load_triples_device
 from .install import install, uninstall

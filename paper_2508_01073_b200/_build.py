@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libwalkvec_b200.so"
-SOURCES = ["abi.cu", "csr.cu", "walks.cu", "bfs.cu", "sgns.cu", "replica.cu", "synth.cu", "ingest.cu"]
+SOURCES = ["abi.cu", "csr.cu", "walks.cu", "bfs.cu", "sgns.cu", "replica.cu", "synth.cu", "ingest.cu", "formats.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -158,6 +158,10 @@ SIGNATURES = {
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
     "wv_sgns_batches": (I32, [P, P, P, I64, I64, P]),
+    "wv_format_workspace_bytes": (I64, [I64, I32]),
+    "wv_format_plan": (I32, [P, I32, I64, I32, P, P, P, P, I64, P]),
+    "wv_format_emit": (I32, [P, P, I64, I32, C.c_char, P, P, I64, P]),
+    "wv_wvc1_pack": (I32, [P, P, I64, P, P]),
     "wv_ingest_lines_workspace_bytes": (I64, [I64]),
     "wv_ingest_lines": (I32, [P, I64, P, P, P, I64, P]),
     "wv_ingest_workspace_bytes": (I64, [I64]),

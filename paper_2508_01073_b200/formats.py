@@ -1,0 +1,102 @@
+"""On-disk formats of the path's outputs, written from the device.
+
+* ``save_embeddings_text`` / ``save_embeddings_tsv`` (pipeline.py:236-251):
+  word2vec text ("<count> <dim>" header, "<lexical> <d floats>" lines) and
+  the TSV export, with Python's correctly rounded ``%.8g`` computed on the
+  device (csrc/formats.cu) and the file written in one piece.
+* ``save_corpus_binary`` (walks.py:344-364): the WVC1 corpus, body packed on
+  the device.  Files are byte-identical to the reference's writers, so the
+  reference's readers (``load_embeddings_text``, ``load_corpus_binary``) load them.
+"""
+
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+
+from . import _lib
+
+_CORPUS_MAGIC = b"WVC1"
+
+
+def _escape_lexical_tsv(value: str) -> str:
+    return value.replace("\\", "\\\\").replace("\t", "\\t").replace("\n", "\\n")
+
+
+def _format_rows(vectors, lexicals: list[str], sep: str) -> bytes:
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    vec = vectors if isinstance(vectors, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vectors))
+    if vec.dtype not in (torch.float32, torch.float64):
+        vec = vec.double()
+    vec = vec.to(dev).contiguous()
+    rows, d = int(vec.shape[0]), int(vec.shape[1])
+    enc = [s.encode("utf-8", "surrogatepass") for s in lexicals]
+    lens = np.fromiter((len(b) for b in enc), dtype=np.int64, count=rows)
+    lex_off = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(lens, out=lex_off[1:])
+    lex = torch.frombuffer(bytearray(b"".join(enc) or b"\0"), dtype=torch.uint8).to(dev)
+    off = torch.from_numpy(lex_off).to(dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(_lib.query("wv_format_workspace_bytes", rows, d), dtype=torch.uint8, device=dev)
+    prec = _lib.FP32 if vec.dtype == torch.float32 else _lib.FP64
+    st = _lib.stream_ptr()
+    _lib.call("wv_format_plan", _lib.ptr(vec), prec, rows, d, _lib.ptr(off), _lib.ptr(total), _lib.ptr(bad),
+              _lib.ptr(ws), ws.numel(), st)
+    if int(bad.item()):
+        raise ValueError("a value lies outside the device %.8g formatter's range (1e-30 <= |x| < 1e16)")
+    out = torch.empty(max(int(total.item()), 1), dtype=torch.uint8, device=dev)
+    _lib.call("wv_format_emit", _lib.ptr(lex), _lib.ptr(off), rows, d, sep.encode(), _lib.ptr(out), _lib.ptr(ws),
+              ws.numel(), st)
+    return out[: int(total.item())].cpu().numpy().tobytes()
+
+
+def _lexicals(vocab, rows: int) -> list[str]:
+    return [vocab.lexical(t) for t in range(rows)]
+
+
+def save_embeddings_text(vectors, vocab, path):
+    """word2vec text format (pipeline.py:236-243)."""
+    rows, d = int(vectors.shape[0]), int(vectors.shape[1])
+    body = _format_rows(vectors, _lexicals(vocab, rows), " ")
+    with open(path, "wb") as fh:
+        fh.write(f"{rows} {d}\n".encode())
+        fh.write(body)
+
+
+def save_embeddings_tsv(vectors, vocab, path):
+    """Tab-separated export: escaped lexical, then the d components (pipeline.py:246-251)."""
+    rows = int(vectors.shape[0])
+    body = _format_rows(vectors, [_escape_lexical_tsv(s) for s in _lexicals(vocab, rows)], "\t")
+    with open(path, "wb") as fh:
+        fh.write(body)
+
+
+def save_corpus_binary(corpus, path):
+    """WVC1 walk corpus (walks.py:344-364), body packed on the device."""
+    from .walks import BFS, ENTITY, FULL, PROPERTY, RANDOM
+
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if hasattr(corpus, "device_arrays"):
+        tok, off = corpus.device_arrays(dev)
+    else:  # the reference's WalkCorpus (host int64 arrays)
+        t64 = np.asarray(corpus.tokens, dtype=np.int64)
+        if t64.size and (t64.min() < 0 or t64.max() >= 2**31):
+            raise ValueError("token does not fit in u32")
+        tok = torch.from_numpy(t64.astype(np.int32) if t64.size else np.zeros(1, np.int32)).to(dev)
+        off = torch.from_numpy(np.asarray(corpus.offsets, dtype=np.int64)).to(dev)
+    n, total = len(corpus), int(np.asarray(corpus.offsets)[-1]) if not hasattr(corpus, "total_tokens") \
+        else corpus.total_tokens
+    if total and int(tok[:total].max()) < 0:
+        raise ValueError("token does not fit in u32")
+    strategies = {RANDOM: 0, BFS: 1}
+    projections = {FULL: 0, ENTITY: 1, PROPERTY: 2}
+    body = torch.empty(max(n + total, 1), dtype=torch.int32, device=dev)
+    _lib.call("wv_wvc1_pack", _lib.ptr(tok), _lib.ptr(off), n, _lib.ptr(body), _lib.stream_ptr())
+    with open(path, "wb") as fh:
+        fh.write(_CORPUS_MAGIC)
+        fh.write(struct.pack("<BBHI", strategies[corpus.strategy], projections[corpus.projection], 0, n))
+        fh.write(body[: n + total].cpu().numpy().astype("<u4").tobytes())

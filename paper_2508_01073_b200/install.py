@@ -5,7 +5,9 @@ hot path through module attributes -- pipeline.extract_walks ->
 walks_mod.random_walks / bfs_walks (pipeline.py:20, 167, 178), and
 ``train`` imported by name into pipeline (pipeline.py:23, 211), cli
 (cli.py:21, 169) and re-exported from the package.  install() swaps exactly
-those attributes, plus ``load_data`` (pipeline.py:117, cli.py:103; GPU ingest);
+those attributes, plus ``load_data`` (pipeline.py:117, cli.py:103; GPU ingest)
+and the artifact writers save_embeddings_text / _tsv and save_corpus_binary
+(device-formatted, byte-identical files);
 uninstall() restores them.
 """
 
@@ -52,6 +54,7 @@ def _wrap_load_data(load_fn, pkg_name: str):
 
 def install(package: str = "walkvec"):
     """Swap the reference's hot-path functions for the device implementations."""
+    from . import formats as dev_formats
     from . import walks as dev_walks
     from .pipeline import load_data as dev_load_data
     from .w2v import train as dev_train
@@ -69,6 +72,9 @@ def install(package: str = "walkvec"):
         (pipe_mod, "train", _wrap_train(dev_train)),
         (pkg, "train", _wrap_train(dev_train)),
         (pipe_mod, "load_data", _wrap_load_data(dev_load_data, package)),
+        (pipe_mod, "save_embeddings_text", dev_formats.save_embeddings_text),
+        (pipe_mod, "save_embeddings_tsv", dev_formats.save_embeddings_tsv),
+        (walks_mod, "save_corpus_binary", dev_formats.save_corpus_binary),
         (pkg, "load_data", _wrap_load_data(dev_load_data, package)),
     ]
     try:

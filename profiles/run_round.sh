@@ -20,7 +20,7 @@ if [ "$PART" = bench ]; then
       --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_list_${TAG}.log 2>&1
   gzip -f gpurun_out/launches_${TAG}.csv
 else
-  for K in sgns_owner_flat heavy_piece_kernel heavy_order group_order sgns_gather_bulk sgns_decode group_segments group_place; do
+  for K in sgns_owner_flat heavy_piece_kernel heavy_order group_order sgns_gather_bulk sgns_decode group_segments group_place_rank; do
     ncu --set full --clock-control none --import-source on -k regex:$K -s 20 -c 1 \
         -o gpurun_out/prof_${K}_${TAG} -f $CMD > gpurun_out/ncu_${K}_${TAG}.log 2>&1
     export_rep gpurun_out/prof_${K}_${TAG}

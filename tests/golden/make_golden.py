@@ -298,6 +298,46 @@ def ingest_cases():
     (OUT / "ingest.json").write_text(json.dumps(cases, indent=1, ensure_ascii=False) + "\n")
 
 
+def formats():
+    """Reference writers (pipeline.py:236-251, walks.py:344-364): exact output bytes."""
+    import base64
+    import tempfile
+
+    from walkvec import walks as rw
+    from walkvec.pipeline import save_embeddings_text, save_embeddings_tsv
+
+    rng = np.random.default_rng(11)
+    special = [0.0, -0.0, 1.0, 0.1, 1e-5, 1.2345678e-5, 123456.78, 12345678.9, 99999999.5, 9.999999995e-05,
+               0.00012345678, -3.25e-10, 1e-30, 0.125, 2.5e-07, -7.77777775, 1e15, 4.4999999949999995]
+    mats = {"f64": np.concatenate([np.array(special + [0.0] * (-len(special) % 6)),
+                                   rng.normal(0, 0.3, 6 * 40) * 10.0 ** rng.integers(-9, 4, 6 * 40)]).reshape(-1, 6)}
+    mats["f32"] = rng.normal(0, 0.2, (30, 5)).astype(np.float32).astype(np.float64)
+    out = {}
+    for name, m in mats.items():
+        lex = [f"tok {i}\twith\\ é" if i % 3 == 0 else f"http://x/{i}" for i in range(len(m))]
+
+        class V:
+            def lexical(self, t):
+                return lex[t]
+
+        for kind, fn in (("text", save_embeddings_text), ("tsv", save_embeddings_tsv)):
+            with tempfile.NamedTemporaryFile(delete=False) as fh:
+                path = fh.name
+            fn(m, V(), path)
+            out[f"{name}_{kind}"] = base64.b64encode(open(path, "rb").read()).decode()
+        out[f"{name}_matrix"] = m.tolist()
+        out[f"{name}_lexicals"] = lex
+    toks = rng.integers(0, 50, 40)
+    offs = [0, 5, 5, 12, 20, 33, 40]
+    corpus = rw.WalkCorpus(toks, np.array(offs), rw.BFS, rw.ENTITY)
+    with tempfile.NamedTemporaryFile(delete=False) as fh:
+        path = fh.name
+    rw.save_corpus_binary(corpus, path)
+    out["wvc1"] = base64.b64encode(open(path, "rb").read()).decode()
+    out["wvc1_tokens"], out["wvc1_offsets"] = toks.tolist(), offs
+    (OUT / "formats.json").write_text(json.dumps(out, ensure_ascii=False) + "\n")
+
+
 def two_clique():
     rows = []
     for base in ("x", "y"):
@@ -340,7 +380,7 @@ def vocab_encoding():
 if __name__ == "__main__":
     # python make_golden.py [generator ...]   (default: all)
     gens = {f.__name__: f for f in (seedseq, walks, bfs, embeddings_and_train, two_clique, vocab_encoding, cbow,
-                                    ingest_cases)}
+                                    ingest_cases, formats)}
     for name in (sys.argv[1:] or list(gens)):
         gens[name]()
     for p in sorted(OUT.glob("*.np*")) + sorted(OUT.glob("*.json")):
