@@ -1167,7 +1167,7 @@ __device__ __forceinline__ uint2 slot_entry(uint32_t v, bool side_out, int64_t B
 // ready list.  Runs on the side stream with the grouping (off the critical
 // path once batches are pipelined).  ci = 0xffffffff marks an input-side
 // contribution (G row, coefficient 1).
-__global__ void group_order(const Segment* __restrict__ segs, const uint32_t* __restrict__ gctr,
+__global__ void group_order(Segment* __restrict__ segs, const uint32_t* __restrict__ gctr,
                             const uint32_t* __restrict__ list, uint2* __restrict__ ents, int64_t V, int64_t B, int k,
                             SlotMap sm) {
   const uint32_t nl = *(volatile const uint32_t*)(gctr + GC_LIGHT);
@@ -1186,6 +1186,12 @@ __global__ void group_order(const Segment* __restrict__ segs, const uint32_t* __
         sl[j - 1] = min(a, b);
         sl[j] = max(a, b);
       }
+    }
+    if (sg.len == 1) {  // the common case: the entry rides in the segment record (start, pad)
+      const uint2 e = slot_entry(sl[0], side_out, B, k, sm);
+      segs[i].start = e.x;
+      segs[i].pad = e.y;
+      continue;
     }
 #pragma unroll
     for (int q = 0; q < kLightMax; ++q) {
@@ -1749,7 +1755,8 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
       const bool side_out = sg[u].key >= (uint32_t)A.V;
       const T* srcb = (side_out ? U : G) + (int64_t)cr[u] * EPC;
       for (uint32_t q = 0; q < sg[u].len; ++q) {
-        const uint2 en = __ldg(A.ents + sg[u].start + q);
+        // single-contribution rows carry their entry in the segment record (group_order)
+        const uint2 en = sg[u].len == 1 ? make_uint2(sg[u].start, sg[u].pad) : __ldg(A.ents + sg[u].start + q);
         const Chunk<T, EPC> x = ld_chunk<T, EPC>(srcb + (int64_t)en.x * d);
         if (side_out) {
           const T c = __ldg(coef + en.y);
