@@ -563,10 +563,9 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
   const T invB = (T)1 / (T)(A.Bn > 0 ? A.Bn : B);
   const int64_t stride = (int64_t)gridDim.x * kBulkWarps;
   int64_t b = blockIdx.x * (int64_t)kBulkWarps + warp;
-  auto issue = [&](int64_t pb, int stage) {
+  auto row_of = [&](int64_t pb) -> int32_t { return (lane < R && pb < B) ? __ldg(A.idx + pb * R + lane) : -1; };
+  auto issue = [&](int64_t pb, int stage, int32_t r) {
     T* dst = ring + (size_t)stage * R * d;
-    int32_t r = -1;
-    if (lane < R) r = __ldg(A.idx + pb * R + lane);
     const uint32_t valid = __ballot_sync(0xffffffffu, lane < R && r >= 0);  // CBOW: masked context columns
     if (lane == 0) mbar_arrive_expect_tx(mybar + stage, row_bytes * (uint32_t)__popc(valid));
     __syncwarp();
@@ -578,16 +577,20 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
   // prologue: the first kBulkStages - 1 pairs
 #pragma unroll
   for (int st = 0; st < kBulkStages - 1; ++st)
-    if (b + st * stride < B) issue(b + st * stride, st);
+    if (b + st * stride < B) issue(b + st * stride, st, row_of(b + st * stride));
   double loss_acc = 0.0;
   uint32_t phase = 0u;  // bit per stage
+  // row indices of the next pair to issue, loaded one iteration ahead so the
+  // copies are issued without waiting on the index load
+  int32_t r_next = row_of(b + (int64_t)(kBulkStages - 1) * stride);
   for (int it = 0; b < B; ++it, b += stride) {
     const int stage = it % kBulkStages;
     const int64_t nb = b + (int64_t)(kBulkStages - 1) * stride;
     if (nb < B) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(nb, (it + kBulkStages - 1) % kBulkStages);
+      issue(nb, (it + kBulkStages - 1) % kBulkStages, r_next);
     }
+    r_next = row_of(nb + stride);
     while (!mbar_try_wait(mybar + stage, (phase >> stage) & 1u)) {
     }
     phase ^= 1u << stage;
