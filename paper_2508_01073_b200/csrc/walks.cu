@@ -114,10 +114,10 @@ struct Walker {
 // (offsets -> packed edge) overlap.  Rows are staged in shared memory and
 // written with 16-byte stores.
 #ifndef WV_WALK_MINB
-#define WV_WALK_MINB 1
+#define WV_WALK_MINB 4
 #endif
 template <int RNG, int WPT>
-__global__ void __launch_bounds__(kWalkThreads, WV_WALK_MINB) random_walk_kernel(WalkParams P,
+__global__ void __launch_bounds__(kWalkThreads, RNG == WV_RNG_PCG64 ? WV_WALK_MINB : 1) random_walk_kernel(WalkParams P,
                                                                               const PcgJump* __restrict__ jrows) {
   extern __shared__ int32_t stage[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
