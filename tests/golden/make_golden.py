@@ -338,6 +338,40 @@ def formats():
     (OUT / "formats.json").write_text(json.dumps(out, ensure_ascii=False) + "\n")
 
 
+def pipeline_cases():
+    """Reference load_data + fit_transform end to end (pipeline.py:117-219) on a small .nt graph."""
+    import tempfile
+
+    from walkvec.pipeline import PipelineConfig, fit_transform, load_data
+
+    rng = np.random.default_rng(8)
+    lines = []
+    for _ in range(400):
+        u, v, p_ = int(rng.integers(0, 60)), int(rng.integers(0, 60)), int(rng.integers(0, 5))
+        lines.append(f"<http://kg/e{u}> <http://kg/p{p_}> <http://kg/e{v}> .")
+    lines += ['<http://kg/e1> <http://kg/label> "one"@en .', "_:b <http://kg/p1> <http://kg/e2> ."]
+    text = "\n".join(lines) + "\n"
+    with tempfile.NamedTemporaryFile("w", suffix=".nt", delete=False) as fh:
+        fh.write(text)
+    configs = {
+        "sg_random": dict(walk_depth=3, walk_number=6, vector_size=8, epochs=2, min_count=1, window_size=2,
+                          negative_samples=3, batch_size=128),
+        "cbow_bfs_entity": dict(walk_strategy="bfs", walk_depth=2, embedding_model="cbow", vector_size=8, epochs=1,
+                                min_count=2, window_size=2, batch_size=64, projection="entity"),
+        "sg_random_dupfree_property": dict(walk_depth=4, walk_number=5, duplicate_free=True, vector_size=6,
+                                           epochs=1, min_count=1, window_size=3, negative_samples=2,
+                                           projection="property", batch_size=100),
+    }
+    out = {"text": text, "cases": {}}
+    for name, kw in configs.items():
+        vocab, edges = load_data(fh.name)
+        table = fit_transform(edges, vocab, PipelineConfig(**kw))
+        out["cases"][name] = dict(cfg=kw, lexicals=vocab.lexical_of, vectors=table.vectors.tolist(),
+                                  losses=list(table.losses), trained=table.trained_mask.tolist(),
+                                  frequency=vocab.frequency.tolist())
+    (OUT / "pipeline.json").write_text(json.dumps(out) + "\n")
+
+
 def two_clique():
     rows = []
     for base in ("x", "y"):
@@ -380,7 +414,7 @@ def vocab_encoding():
 if __name__ == "__main__":
     # python make_golden.py [generator ...]   (default: all)
     gens = {f.__name__: f for f in (seedseq, walks, bfs, embeddings_and_train, two_clique, vocab_encoding, cbow,
-                                    ingest_cases, formats)}
+                                    ingest_cases, formats, pipeline_cases)}
     for name in (sys.argv[1:] or list(gens)):
         gens[name]()
     for p in sorted(OUT.glob("*.np*")) + sorted(OUT.glob("*.json")):
