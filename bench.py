@@ -126,10 +126,13 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
-        backend = "nccl"
+        # BENCH_DIST_BACKEND=gloo exercises the multi-rank path on a single GPU
+        # (ranks share device local % device_count); NCCL is the real path
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         import torch
 
         if torch.cuda.is_available():
+            local = local % torch.cuda.device_count()
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return rank, world, local
