@@ -1177,6 +1177,12 @@ __global__ void group_order(Segment* __restrict__ segs, const uint32_t* __restri
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
     const Segment sg = segs[i];
     const bool side_out = sg.key >= (uint32_t)V;
+    if (sg.len == 1) {  // the common case: the entry rides in the segment record (start, pad)
+      const uint2 e = slot_entry(list[sg.start], side_out, B, k, sm);
+      segs[i].start = e.x;
+      segs[i].pad = e.y;
+      continue;
+    }
     uint32_t sl[kLightMax];
 #pragma unroll
     for (int q = 0; q < kLightMax; ++q) sl[q] = q < (int)sg.len ? list[sg.start + q] : 0xffffffffu;
@@ -1189,12 +1195,6 @@ __global__ void group_order(Segment* __restrict__ segs, const uint32_t* __restri
         sl[j - 1] = min(a, b);
         sl[j] = max(a, b);
       }
-    }
-    if (sg.len == 1) {  // the common case: the entry rides in the segment record (start, pad)
-      const uint2 e = slot_entry(sl[0], side_out, B, k, sm);
-      segs[i].start = e.x;
-      segs[i].pad = e.y;
-      continue;
     }
 #pragma unroll
     for (int q = 0; q < kLightMax; ++q) {
