@@ -219,3 +219,21 @@ def test_cbow_device_mode_deterministic_and_learns(golden, wv):
     b, lb = wv.train(corpus, int(g["train_V"]), cfg, 3)
     assert np.array_equal(a.input_matrix, b.input_matrix) and la == lb
     assert la[-1] < la[0]
+
+
+def test_large_batch_replay_matches_oracle(wv):
+    """Batches beyond the shared-memory slot bitmap (> 393,216 items): heavy rows take the
+    CTA radix-sort path; fp64 replay of the reference streams still matches the oracle."""
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("barabasi", 4000, m=4, predicates=12, seed=5)
+    graph = wv.build_graph(edges, V)
+    corpus = wv.random_walks(graph, ents, walk_depth=4, walk_number=20, rng_seed=3)
+    cfg = wv.TrainConfig(min_count=1, vector_size=8, epochs=1, window_size=3, negative_samples=5,
+                         batch_size=70_000)
+    model, losses = wv.train(corpus, V, cfg, 42, precision="fp64", pairs="numpy")
+    ref = ov.train(corpus.tokens, corpus.offsets, V, 8, 3, 5, 0.01, 1, 1, 42, batch=70_000)
+    assert 70_000 * 7 > 393_216
+    np.testing.assert_allclose(model.input_matrix, ref["inp"], rtol=0, atol=1e-10)
+    np.testing.assert_allclose(model.output_matrix, ref["out"], rtol=0, atol=1e-10)
+    np.testing.assert_allclose(losses, ref["losses"], rtol=1e-10)
