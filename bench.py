@@ -474,14 +474,16 @@ def run_ours(args, rank, world, local):
     batch_bytes = pair_bytes + owner_bytes
     batch_ms = ph.get("batch", float("nan"))
     # ncu DRAM traffic per launch of the owner phase's kernels (same batch geometry), newest capture
-    traffic, traffic_src = None, None
+    traffic, traffic_src, batch_traffic = None, None, None
     tfs = sorted((ROOT / "profiles").glob("traffic_*.json"))
     if tfs:
         t_ = json.loads(tfs[-1].read_text())
-        parts = [k_ for k_ in ("sgns_owner_flat", "heavy_piece") if k_ in t_]
-        if parts:
-            traffic = sum(t_[k_]["dram_bytes"] for k_ in parts)
-            traffic_src = f"{tfs[-1].relative_to(ROOT)}: ncu --set full dram__bytes_read+write of {' + '.join(parts)}"
+        owner_parts = [k_ for k_ in t_ if k_.startswith("sgns_owner") or k_.startswith("heavy_piece")]
+        if owner_parts:
+            traffic = sum(t_[k_]["dram_bytes"] for k_ in owner_parts)
+            traffic_src = (f"{tfs[-1].relative_to(ROOT)}: ncu --set full dram__bytes_read+write of "
+                           f"{' + '.join(sorted(owner_parts))}")
+        batch_traffic = sum(v_["dram_bytes"] for k_, v_ in t_.items() if k_ != "random_walk_kernel")
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
         "frac": kern[dom]["frac"], "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
@@ -489,7 +491,13 @@ def run_ours(args, rank, world, local):
         "kernels": kern,
         "sgns_batch": {"bytes": batch_bytes, "ms": batch_ms, "gbs": batch_bytes / (batch_ms * 1e-3) / 1e9,
                        "frac": batch_bytes / (batch_ms * 1e-3) / 1e9 / peak, "batch_pairs": B,
-                       "unique_rows_per_batch": U},
+                       "unique_rows_per_batch": U,
+                       "dram_traffic": batch_traffic,
+                       "frac_of_measured_traffic": (batch_traffic / (batch_ms * 1e-3) / 1e9 / peak
+                                                    if batch_traffic else None)},
+        # the same kernel against its measured DRAM bytes (the algorithmic figure counts a row
+        # gathered by the pair phase and then updated by the Adam phase twice)
+        "frac_of_measured_traffic": (traffic / (kern[dom]["ms"] * 1e-3) / 1e9 / peak if traffic else None),
         "note": "achieved = SURVEY §8d algorithmic bytes per launch / mean CUDA-event launch time. walk: events "
                 "around the walk kernel in the timed steps; SGNS phases: CUDA events around the phases of every 16th "
                 "batch of one extra step right after the timed region, run eagerly (event nodes inside CUDA graphs "
