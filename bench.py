@@ -484,6 +484,9 @@ def run_ours(args, rank, world, local):
             traffic_src = (f"{tfs[-1].relative_to(ROOT)}: ncu --set full dram__bytes_read+write of "
                            f"{' + '.join(sorted(owner_parts))}")
         batch_traffic = sum(v_["dram_bytes"] for k_, v_ in t_.items() if k_ != "random_walk_kernel")
+        if "random_walk_kernel" in t_:  # CSR lookups: ncu DRAM bytes and L2 hit rate of the walk kernel
+            kern["walk"]["ncu_dram_bytes"] = t_["random_walk_kernel"]["dram_bytes"]
+            kern["walk"]["ncu_l2_hit_rate_pct"] = t_["random_walk_kernel"].get("l2_hit_rate_pct")
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
         "frac": kern[dom]["frac"], "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,

@@ -23,6 +23,8 @@ for p in sorted((ROOT / "gpurun_out").glob(f"prof_*_{tag}.raw.csv.gz")):
     k = p.name[len("prof_"):-len(f"_{tag}.raw.csv.gz")]
     out[k] = {"dram_bytes": b, "duration_us": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
               (1e-3 if d["gpu__time_duration.sum"][1] == "nsecond" else 1.0),
+              "l2_hit_rate_pct": float(d["lts__t_sector_hit_rate.pct"][0].replace(",", ""))
+              if "lts__t_sector_hit_rate.pct" in d else None,
               "kernel": d["Kernel Name"][0][:120]}
 (ROOT / "profiles" / f"traffic_{tag}.json").write_text(json.dumps(out, indent=1) + "\n")
 print(json.dumps(out, indent=1))
