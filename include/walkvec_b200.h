@@ -331,6 +331,15 @@ int64_t wv_barabasi_edge_count(int64_t n, int m);
 int64_t wv_barabasi_workspace_bytes(int64_t n, int m);
 int wv_gen_barabasi(int64_t n, int m, uint64_t seed, int64_t* src, int64_t* dst, void* ws, int64_t ws_bytes,
                     void* stream);
+/* benchgen.gen_erdos_renyi (benchgen.py:112-127) and gen_uniform_attachment
+ * (:130-149) semantics with counter-based draws: edges in the reference's order
+ * (row-major pairs; per vertex ascending distinct targets).  src = dst = NULL
+ * returns the edge count in *n_edges (device int64); then call with buffers. */
+int64_t wv_gen_rows_workspace_bytes(int64_t n);
+int wv_gen_erdos_renyi(int64_t n, double p, uint64_t seed, int64_t* src, int64_t* dst, int64_t* n_edges, void* ws,
+                       int64_t ws_bytes, void* stream);
+int wv_gen_uniform_attachment(int64_t n, int m, uint64_t seed, int64_t* src, int64_t* dst, int64_t* n_edges,
+                              void* ws, int64_t ws_bytes, void* stream);
 /* First-occurrence token encoding of integer triples (ingest.build_vocabulary,
  * ingest.py:368-396, over benchgen.assign_predicates' "v{u}"/"P{k}" triples,
  * benchgen.py:152-161).  Keys: entity u -> u, predicate k -> n_entities + k.

@@ -158,6 +158,9 @@ SIGNATURES = {
     "wv_sgns_batch": (I32, [P, P, P, I64, P]),
     "wv_sgns_batch_phases": (I32, [P, P, P, I64, I32, P]),
     "wv_sgns_batches": (I32, [P, P, P, I64, I64, P]),
+    "wv_gen_rows_workspace_bytes": (I64, [I64]),
+    "wv_gen_erdos_renyi": (I32, [I64, C.c_double, U64, P, P, P, P, I64, P]),
+    "wv_gen_uniform_attachment": (I32, [I64, I32, U64, P, P, P, P, I64, P]),
     "wv_format_workspace_bytes": (I64, [I64, I32]),
     "wv_format_plan": (I32, [P, I32, I64, I32, P, P, P, P, I64, P]),
     "wv_format_emit": (I32, [P, P, I64, I32, C.c_char, P, P, I64, P]),

@@ -164,6 +164,93 @@ __global__ void enc_edges(const int64_t* __restrict__ src, const int64_t* __rest
     out[p] = token_of_key[stream_key(src, pred, dst, n_entities, p)];
 }
 
+// ------------------------------------------------ Erdos-Renyi, uniform --
+// benchgen.gen_erdos_renyi (benchgen.py:112-127): ordered pair (u, v), u != v,
+// present with probability p, edges in row-major (u, v) order; and
+// benchgen.gen_uniform_attachment (benchgen.py:130-149): vertex v >= 1 draws m
+// targets uniformly from [0, v), duplicates collapse, targets ascending.
+// Counter-based draws (Philox4x32 keyed by seed), not numpy's stream.
+__device__ __forceinline__ uint64_t gen_draw(uint64_t seed, uint64_t a, uint64_t b, uint32_t tag) {
+  uint32_t c[4] = {(uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32) ^ tag};
+  philox4x32_10(c, (uint32_t)seed ^ 0x5bd1e995u, (uint32_t)(seed >> 32) ^ 0x27d4eb2fu);
+  return ((uint64_t)c[1] << 32) | c[0];
+}
+
+__device__ __forceinline__ bool er_cell(uint64_t seed, int64_t u, int64_t v, double p) {
+  return u != v && (double)(gen_draw(seed, (uint64_t)u, (uint64_t)v, 0x45u) >> 11) * (1.0 / 9007199254740992.0) < p;
+}
+
+// block per row: count (pass 0) or emit in column order (pass 1)
+__global__ void er_rows(int64_t n, double p, uint64_t seed, int pass, int64_t* __restrict__ row_count,
+                        const int64_t* __restrict__ row_off, int64_t* __restrict__ src, int64_t* __restrict__ dst) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t run;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t u = blockIdx.x; u < n; u += gridDim.x) {
+    if (threadIdx.x == 0) run = pass ? row_off[u] : 0;
+    __syncthreads();
+    for (int64_t v0 = 0; v0 < n; v0 += blockDim.x) {
+      const int64_t v = v0 + threadIdx.x;
+      const bool hit = v < n && er_cell(seed, u, v, p);
+      const uint32_t m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) warp_tot[warp] = __popc(m);
+      __syncthreads();
+      if (pass && hit) {
+        int64_t before = run;
+        for (int w = 0; w < warp; ++w) before += warp_tot[w];
+        before += __popc(m & ((1u << lane) - 1u));
+        src[before] = u;
+        dst[before] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int w = 0; w < nw; ++w) run += warp_tot[w];
+      __syncthreads();
+    }
+    if (!pass && threadIdx.x == 0) row_count[u] = run;
+    __syncthreads();
+  }
+}
+
+// thread per vertex: the sorted distinct targets of vertex v (m <= 64)
+__device__ int ua_targets(uint64_t seed, int64_t v, int m, int64_t* t) {
+  for (int j = 0; j < m; ++j) t[j] = (int64_t)mulhi64(gen_draw(seed, (uint64_t)v, (uint64_t)j, 0x55u), (uint64_t)v);
+  for (int i = 1; i < m; ++i) {
+    const int64_t x = t[i];
+    int j = i - 1;
+    while (j >= 0 && t[j] > x) {
+      t[j + 1] = t[j];
+      --j;
+    }
+    t[j + 1] = x;
+  }
+  int k = 0;
+  for (int i = 0; i < m; ++i)
+    if (i == 0 || t[i] != t[i - 1]) t[k++] = t[i];
+  return k;
+}
+
+__global__ void ua_vertices(int64_t n, int m, uint64_t seed, int pass, int64_t* __restrict__ count,
+                            const int64_t* __restrict__ off, int64_t* __restrict__ src, int64_t* __restrict__ dst) {
+  int64_t t[64];
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (v == 0) {
+      if (!pass) count[0] = 0;
+      continue;
+    }
+    const int k = ua_targets(seed, v, m, t);
+    if (!pass) {
+      count[v] = k;
+      continue;
+    }
+    const int64_t o = off[v];
+    for (int j = 0; j < k; ++j) {
+      src[o + j] = v;
+      dst[o + j] = t[j];
+    }
+  }
+}
+
 static inline unsigned grid_of(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 64) g = 148 * 64;
@@ -276,6 +363,52 @@ int wv_encode_triples(const int64_t* src, const int64_t* preds, const int64_t* d
     WV_LAUNCH_CHECK();
   }
   return 0;
+}
+
+// Erdos-Renyi / uniform attachment on the device: call with src = dst = NULL to
+// get the edge count (*n_edges, device int64), then again with buffers of that size.
+int64_t wv_gen_rows_workspace_bytes(int64_t n) {
+  using namespace wv;
+  return al256(n * 8) * 2 + al256(scan_tiles(n) * 8) + 256;
+}
+
+static int gen_rows(int kind, int64_t n, double p, int m, uint64_t seed, int64_t* src, int64_t* dst,
+                    int64_t* n_edges, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  using namespace wv;
+  WV_CHECK_ARG(ws_bytes >= wv_gen_rows_workspace_bytes(n), "workspace too small");
+  char* w = (char*)ws;
+  int64_t* cnt = (int64_t*)w;
+  w += al256(n * 8);
+  int64_t* off = (int64_t*)w;
+  w += al256(n * 8);
+  int64_t* scan_ws = (int64_t*)w;
+  if (kind == 0)
+    er_rows<<<grid_of(n, 1), 256, 0, st>>>(n, p, seed, 0, cnt, nullptr, nullptr, nullptr);
+  else
+    ua_vertices<<<grid_of(n, 128), 128, 0, st>>>(n, m, seed, 0, cnt, nullptr, nullptr, nullptr);
+  WV_LAUNCH_CHECK();
+  WV_CUDA((excl_scan<int64_t, int64_t>(cnt, n, off, n_edges, scan_ws, st)));
+  if (src == nullptr) return 0;
+  if (kind == 0)
+    er_rows<<<grid_of(n, 1), 256, 0, st>>>(n, p, seed, 1, nullptr, off, src, dst);
+  else
+    ua_vertices<<<grid_of(n, 128), 128, 0, st>>>(n, m, seed, 1, nullptr, off, src, dst);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int wv_gen_erdos_renyi(int64_t n, double p, uint64_t seed, int64_t* src, int64_t* dst, int64_t* n_edges, void* ws,
+                       int64_t ws_bytes, void* stream) {
+  WV_CHECK_ARG(n >= 1, "n must be >= 1");
+  WV_CHECK_ARG(p > 0.0 && p < 1.0, "p must be in (0, 1)");
+  return gen_rows(0, n, p, 0, seed, src, dst, n_edges, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int wv_gen_uniform_attachment(int64_t n, int m, uint64_t seed, int64_t* src, int64_t* dst, int64_t* n_edges,
+                              void* ws, int64_t ws_bytes, void* stream) {
+  WV_CHECK_ARG(n >= 2, "n must be >= 2");
+  WV_CHECK_ARG(m >= 1 && m <= 64, "m must be in [1, 64]");
+  return gen_rows(1, n, 0.0, m, seed, src, dst, n_edges, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -146,6 +146,38 @@ def device_barabasi_edges(n: int, m: int, seed: int = 7, device=None):
     return src, dst
 
 
+def _device_rows(fn: str, n: int, arg, seed: int, device=None):
+    from . import _lib
+
+    torch = _lib.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ws = torch.empty(_lib.query("wv_gen_rows_workspace_bytes", n), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    s = int(seed) & 0xFFFFFFFFFFFFFFFF
+    _lib.call(fn, n, arg, s, None, None, _lib.ptr(cnt), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    E = int(cnt.item())
+    src = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+    dst = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+    _lib.call(fn, n, arg, s, _lib.ptr(src), _lib.ptr(dst), _lib.ptr(cnt), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    return src[:E], dst[:E]
+
+
+def device_erdos_renyi_edges(n: int, p: float, seed: int = 7, device=None):
+    """(src, dst) device tensors: gen_erdos_renyi semantics (benchgen.py:112-127), counter-based draws."""
+    if not 0 < p < 1:
+        raise ValueError("p must be in (0, 1)")
+    return _device_rows("wv_gen_erdos_renyi", int(n), float(p), seed, device)
+
+
+def device_uniform_attachment_edges(n: int, m: int = 10, seed: int = 7, device=None):
+    """(src, dst) device tensors: gen_uniform_attachment semantics (benchgen.py:130-149)."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    if not 1 <= m <= 64:
+        raise ValueError("m must be in [1, 64]")
+    return _device_rows("wv_gen_uniform_attachment", int(n), int(m), seed, device)
+
+
 def device_encode(src, preds, dst, n_entities: int, n_predicates: int):
     """First-occurrence encoding on the device -> (edges (E,3), vocab_size, entity_tokens, predicate_tokens).
 
@@ -186,10 +218,9 @@ def device_synthetic_kg(model: str, n: int, m: int = 10, predicates: int = 10, s
     if model == "barabasi":
         src, dst = device_barabasi_edges(n, m, seed, device)
     elif model == "erdos_renyi":
-        e2 = erdos_renyi_edges(n, p, seed)
-        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        src = torch.from_numpy(np.ascontiguousarray(e2[:, 0])).to(dev)
-        dst = torch.from_numpy(np.ascontiguousarray(e2[:, 1])).to(dev)
+        src, dst = device_erdos_renyi_edges(n, p, seed, device)
+    elif model == "uniform_attachment":
+        src, dst = device_uniform_attachment_edges(n, m, seed, device)
     else:
         raise ValueError(f"unknown model {model!r}")
     picks = torch.from_numpy(predicate_picks(int(src.numel()), predicates, seed)).to(src.device)

@@ -93,3 +93,39 @@ def test_device_synthetic_kg_cfg1_shape(wv):
     g = wv.build_graph(edges, V)
     deg = np.diff(g.row_offsets)
     assert deg.max() == 5
+
+
+def test_device_erdos_renyi_structure(wv):
+    """gen_erdos_renyi semantics: no self loops, row-major order, edge count ~ Binomial(n(n-1), p)."""
+    from paper_2508_01073_b200.synth import device_erdos_renyi_edges
+
+    n, p = 15_000, 0.001378
+    src, dst = device_erdos_renyi_edges(n, p, seed=7)
+    s, d = src.cpu().numpy(), dst.cpu().numpy()
+    mean, sd = n * (n - 1) * p, (n * (n - 1) * p * (1 - p)) ** 0.5
+    assert abs(len(s) - mean) < 6 * sd
+    assert (s != d).all() and (s >= 0).all() and (d < n).all()
+    key = s * n + d
+    assert (np.diff(key) > 0).all()  # strictly row-major, no duplicates
+    s2, d2 = device_erdos_renyi_edges(n, p, seed=7)
+    assert np.array_equal(s2.cpu().numpy(), s)
+
+
+def test_device_uniform_attachment_structure(wv):
+    """gen_uniform_attachment semantics: per vertex v >= 1, distinct ascending targets in [0, v),
+    at most min(m, v) of them; the expected count matches m uniform draws with collisions."""
+    from paper_2508_01073_b200.synth import device_uniform_attachment_edges
+
+    n, m = 50_000, 10
+    src, dst = device_uniform_attachment_edges(n, m, seed=3)
+    s, d = src.cpu().numpy(), dst.cpu().numpy()
+    assert (d < s).all() and (s >= 1).all()
+    assert (np.diff(s) >= 0).all()
+    same = s[1:] == s[:-1]
+    assert (d[1:][same] > d[:-1][same]).all()
+    per = np.bincount(s, minlength=n)
+    v = np.arange(n)
+    assert (per[1:] <= np.minimum(m, v[1:])).all()
+    # E[distinct] = v (1 - (1 - 1/v)^m)
+    expect = (v[1:] * (1 - (1 - 1 / v[1:]) ** m)).sum()
+    assert abs(per.sum() - expect) / expect < 0.01
