@@ -50,6 +50,7 @@ struct WalkParams {
   const uint64_t* edges;
   const int64_t* roots;
   int64_t walk_number;
+  double inv_walk_number;
   int64_t work_begin;  // global index of the first walker of this launch
   int64_t work_count;  // walkers in this launch
   int64_t last_shard;  // global shard index of the final (possibly partial) shard
@@ -160,7 +161,12 @@ __global__ void __launch_bounds__(kWalkThreads, RNG == WV_RNG_PCG64 ? WV_WALK_MI
     W[q].last = (s == P.last_shard);
     jr[q] = jrows + W[q].i;  // i + 1 steps
     if (W[q].alive) {
-      W[q].cur = P.roots[w / P.walk_number];
+      // root index w / walk_number via a float64 reciprocal and a one-step correction
+      // (a 64-bit integer division costs ~70 instructions per walker)
+      int64_t ri = (int64_t)((double)w * P.inv_walk_number);
+      if (ri * P.walk_number > w) --ri;
+      else if ((ri + 1) * P.walk_number <= w) ++ri;
+      W[q].cur = P.roots[ri];
       my[0] = (int32_t)W[q].cur;
       W[q].len = 1;
     }
@@ -400,6 +406,7 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, in
   P.edges = packed_edges;
   P.roots = roots;
   P.walk_number = walk_number;
+  P.inv_walk_number = 1.0 / (double)walk_number;
   P.work_begin = work_begin;
   P.work_count = work_count;
   P.last_shard = (total - 1) / kShard;
