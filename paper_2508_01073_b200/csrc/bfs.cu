@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kBfsThreads) bfs_kernel(BfsArgs A) {
   uint32_t* s_hk = s_hash;
   uint32_t* s_hv = s_hash + kSmemCap;
   __shared__ int s_inserted, s_overflow;
-  __shared__ int64_t s_total, s_chunk_tot, s_ndisc, s_f0, s_nleaf;
+  __shared__ int64_t s_total, s_chunk_tot, s_ndisc, s_f0;
   const int tid = threadIdx.x;
   uint32_t* hk = SMEM ? s_hk : A.g_hkey + (int64_t)blockIdx.x * A.hash_cap;
   uint32_t* hv = SMEM ? s_hv : A.g_hval + (int64_t)blockIdx.x * A.hash_cap;

@@ -522,7 +522,6 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 #endif
 constexpr int kBulkWarps = WV_GATHER_WARPS;
 constexpr int kBulkStages = WV_GATHER_STAGES;  // pairs in flight per warp
-constexpr int kBulkThreads = kBulkWarps * 32;
 
 // Phase 1b (default path): warp per pair with the 2+k rows fetched by
 // cp.async.bulk into a per-warp two-stage shared-memory ring.  Lane j issues
@@ -1872,7 +1871,7 @@ template <typename T, int EPC, int MAXC>
 #endif
 __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kernel(OwnerArgs A) {
   constexpr int W = kHeavyThreads / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* part = reinterpret_cast<T*>(smem_raw);  // [W][d]
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem_raw + (size_t)W * A.d * sizeof(T));
   const uint32_t bitmap_words = heavy_bitmap_words(A.n_items);
@@ -2031,7 +2030,7 @@ __host__ __device__ __forceinline__ int64_t max_pieces(int64_t items) {
 }
 
 __global__ void __launch_bounds__(kHeavyThreads) heavy_order(OwnerArgs A, uint32_t* gctr, uint2* pieces) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem_raw);
   const uint32_t bitmap_words = heavy_bitmap_words(A.n_items);
   __shared__ uint32_t sort_hist[kHeavyThreads / 32][256];
@@ -2954,8 +2953,7 @@ int wv_pair_index_build(const int64_t* offsets, int64_t n_walks, int window, int
   uint32_t* keys = (uint32_t*)w;
   w += al256(n_walks * 4);
   uint32_t* vals = (uint32_t*)walks_by_class;
-  uint32_t* tmpv = (uint32_t*)w;
-  w += al256(n_walks * 4);
+  w += al256(n_walks * 4);  // (radix scratch values live in rws)
   void* rws = w;
   w += al256(radix_ws_bytes(n_walks, 32));
   uint8_t* head = (uint8_t*)w;
@@ -2965,7 +2963,6 @@ int wv_pair_index_build(const int64_t* offsets, int64_t n_walks, int window, int
   int64_t* cpairs = (int64_t*)w;
   w += al256((n_walks + 1) * 8);
   int64_t* scan_ws = (int64_t*)w;
-  (void)tmpv;
   walk_len_keys<<<grid_for(n_walks, 256), 256, 0, st>>>(offsets, n_walks, keys, vals);
   WV_LAUNCH_CHECK();
   WV_CUDA(radix_sort_pairs(keys, vals, n_walks, 32, rws, st));
