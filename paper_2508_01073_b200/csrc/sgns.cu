@@ -2023,7 +2023,11 @@ __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kerne
 // row's last piece sums the piece partials in piece order and applies RowAdam.
 // The association ((c0 + .. + c31) + (c32 + ..)) is fixed, so results are
 // deterministic run to run.
-constexpr int kPiece = 32;
+#ifndef WV_PIECE
+#define WV_PIECE 32
+#endif
+constexpr int kPiece = WV_PIECE;
+static_assert(kPiece >= 1 && kPiece <= 32, "heavy pieces map one contribution per lane");
 
 __host__ __device__ __forceinline__ int64_t max_pieces(int64_t items) {
   return items / kPiece + items / (kLightMax + 1) + 2;
