@@ -1662,6 +1662,18 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
 #ifndef WV_FLAT_PREFETCH
 #define WV_FLAT_PREFETCH 0
 #endif
+#ifndef WV_FLAT_ASYNC
+#define WV_FLAT_ASYNC 0  // measured slower (smem carve-out shrinks L1; 205 vs 151 us)
+#endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
 template <typename T, int EPC, int MAXC>
 __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc);
@@ -1690,6 +1702,99 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
   const T lr = (T)A.lr;
   const uint32_t total = nseg * C;
   const uint32_t stride = gridDim.x * blockDim.x * kFlatU;
+  if constexpr (WV_FLAT_ASYNC && kFlatU == 1 && EPC * sizeof(T) == 16) {
+    // Two-deep software pipeline: the next item's optimizer state (and its only
+    // contribution row, for single-contribution rows) is copied HBM -> shared
+    // with cp.async while this item is summed and updated, so each thread keeps
+    // two items' loads in flight without holding them in registers.
+    __shared__ __align__(16) uint4 abuf[2][4][256];
+    __shared__ Segment sbuf[2][256];  // the in-flight items' segment records (off the register file)
+    const int tid = threadIdx.x;
+    auto chunk_of = [&](uint32_t i, uint32_t& r) {
+      r = __umulhi(i, A.cmag);
+      int32_t c = (int32_t)(i - r * C);
+      if (c < 0) {
+        --r;
+        c += (int32_t)C;
+      } else if (c >= (int32_t)C) {
+        ++r;
+        c -= (int32_t)C;
+      }
+      return c;
+    };
+    auto issue = [&](uint32_t i, int s) {
+      uint32_t r;
+      const int32_t c = chunk_of(i, r);
+      const Segment sg = A.segs[r];
+      sbuf[s][tid] = sg;
+      const bool so = sg.key >= (uint32_t)A.V;
+      const int64_t row = so ? (int64_t)sg.key - A.V : (int64_t)sg.key;
+      const int64_t o = row * d + (int64_t)c * EPC;
+      cp_async16(&abuf[s][0][tid], (const T*)(so ? A.out : A.in) + o);
+      cp_async16(&abuf[s][1][tid], (const T*)(so ? A.m_out : A.m_in) + o);
+      cp_async16(&abuf[s][2][tid], (const T*)(so ? A.v_out : A.v_in) + o);
+      if (sg.len == 1) cp_async16(&abuf[s][3][tid], (so ? U : G) + (int64_t)sg.start * d + (int64_t)c * EPC);
+      cp_async_commit();
+    };
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    int s = 0;
+    if (i < total) issue(i, 0);
+    for (; i < total; i += stride) {
+      const uint32_t inx = i + stride;
+      if (inx < total)
+        issue(inx, s ^ 1);
+      else
+        cp_async_commit();
+      cp_async_wait<1>();
+      uint32_t rr;
+      const int32_t c = chunk_of(i, rr);
+      const Segment sg = sbuf[s][tid];
+      const bool side_out = sg.key >= (uint32_t)A.V;
+      const int64_t row = side_out ? (int64_t)sg.key - A.V : (int64_t)sg.key;
+      const int64_t o = row * d + (int64_t)c * EPC;
+      Chunk<T, EPC> p = *reinterpret_cast<const Chunk<T, EPC>*>(&abuf[s][0][tid]);
+      Chunk<T, EPC> m = *reinterpret_cast<const Chunk<T, EPC>*>(&abuf[s][1][tid]);
+      Chunk<T, EPC> vv = *reinterpret_cast<const Chunk<T, EPC>*>(&abuf[s][2][tid]);
+      Chunk<T, EPC> g;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) g.v[e] = 0;
+      if (sg.len == 1) {
+        const Chunk<T, EPC> x = *reinterpret_cast<const Chunk<T, EPC>*>(&abuf[s][3][tid]);
+        const T cf = side_out ? __ldg(coef + sg.pad) : T(1);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) g.v[e] = add_rn(g.v[e], side_out ? mul_rn(cf, x.v[e]) : x.v[e]);
+      } else {
+        const T* srcb = (side_out ? U : G) + (int64_t)c * EPC;
+        for (uint32_t q = 0; q < sg.len; ++q) {
+          const uint2 en = __ldg(A.ents + sg.start + q);
+          const Chunk<T, EPC> x = ld_chunk<T, EPC>(srcb + (int64_t)en.x * d);
+          if (side_out) {
+            const T cq = __ldg(coef + en.y);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) g.v[e] = add_rn(g.v[e], mul_rn(cq, x.v[e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) g.v[e] = add_rn(g.v[e], x.v[e]);
+          }
+        }
+      }
+      const AdamBC<T> bc(sg.bc1, sg.bc2);
+      bool changed = false;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g.v[e], bc, lr) != T(0);
+      st_chunk<T, EPC>((T*)(side_out ? A.out : A.in) + o, p);
+      st_chunk<T, EPC>((T*)(side_out ? A.m_out : A.m_in) + o, m);
+      st_chunk<T, EPC>((T*)(side_out ? A.v_out : A.v_in) + o, vv);
+      if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+      if (c == 0) {
+        (side_out ? A.touched_out : A.touched_in)[row] = 1;
+        A.cnt[sg.key] = 0;
+      }
+      s ^= 1;
+    }
+    cp_async_wait<0>();
+    return;
+  }
   for (uint32_t i0 = blockIdx.x * blockDim.x * kFlatU + threadIdx.x; i0 < total; i0 += stride) {
     if (WV_FLAT_PREFETCH > 0) {
       // L2 prefetch of the optimizer-state rows this thread's item will touch
