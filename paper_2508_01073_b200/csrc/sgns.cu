@@ -58,8 +58,11 @@ __device__ __forceinline__ double mad_t(double a, double b, double c) { return _
 __device__ __forceinline__ double exp_t(double a) { return exp(a); }
 
 // ------------------------------------------------------ vector row I/O ----
+// Aligned to its own size (4/8/16 B): every chunk sits at a multiple of EPC
+// elements from an aligned row base, and the alignment lets shared-memory chunk
+// reads compile to one LDS.64/128 instead of EPC conflicting 4-byte LDS.
 template <typename T, int EPC>
-struct Chunk {
+struct alignas(sizeof(T) * EPC) Chunk {
   T v[EPC];
 };
 
