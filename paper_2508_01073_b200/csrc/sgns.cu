@@ -154,6 +154,9 @@ __device__ __forceinline__ void st_chunk_mv(T* p, const Chunk<T, EPC>& c) {
 #ifndef WV_OWNER_P_DEMOTE
 #define WV_OWNER_P_DEMOTE 0
 #endif
+#ifndef WV_OWNER_P_APPLY
+#define WV_OWNER_P_APPLY 0
+#endif
 template <typename T, int EPC>
 __device__ __forceinline__ Chunk<T, EPC> ld_chunk_p(const T* p) {
   if constexpr (WV_OWNER_P_DEMOTE != 0 && EPC * sizeof(T) == 16 && sizeof(T) == 4) {
@@ -1974,6 +1977,11 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
 #pragma unroll
       for (int e = 0; e < EPC; ++e) changed |= adam_elem<T>(p[u].v[e], m[u].v[e], vv[u].v[e], g[u].v[e], bc, lr) != T(0);
       st_chunk_p<T, EPC>((T*)(side_out ? A.out : A.in) + o, p[u]);
+      if (WV_OWNER_P_APPLY) {
+        // hand the gather's evict-last line back to the normal pool once updated
+        const uintptr_t ln = (uintptr_t)((T*)(side_out ? A.out : A.in) + o) & ~(uintptr_t)127;
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(ln) : "memory");
+      }
       st_chunk_mv<T, EPC>((T*)(side_out ? A.m_out : A.m_in) + o, m[u]);
       st_chunk_mv<T, EPC>((T*)(side_out ? A.v_out : A.v_in) + o, vv[u]);
       if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
