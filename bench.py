@@ -47,14 +47,14 @@ DEPTH, WALKS, DIM, WINDOW, NEG, LR, SEED = 8, 100, 200, 5, 5, 0.01, 42
 BUDGET = 1 << 30
 
 
-def workload(roots_per_step: int) -> dict:
+def workload(roots_per_step: int, precision: str = "fp64") -> dict:
     return {
         "workload": "cfg2: BA(1M entities, m=10) -> 9,999,945 triples, 200 predicates; random walks depth 8 x 100/entity "
                     "(reference PCG64 streams, bit-exact corpus); SGNS d200 w5 k5 lr0.01, reference 1 GiB batch rule "
                     f"(23,933 pairs); step = {roots_per_step}-entity root block per GPU, 1 SGNS epoch over its pairs",
         "graph": {"model": "barabasi", "entities": N_ENT, "m": M_BA, "predicates": N_PRED, "gen_seed": GEN_SEED},
         "walks": {"depth": DEPTH, "walks_per_entity": WALKS, "rng": "pcg64"},
-        "sgns": {"dim": DIM, "window": WINDOW, "negatives": NEG, "lr": LR, "batch_rule": "1 GiB", "precision": "fp32"},
+        "sgns": {"dim": DIM, "window": WINDOW, "negatives": NEG, "lr": LR, "batch_rule": "1 GiB", "precision": precision},
         "roots_per_step": roots_per_step,
         "l2": "no flush: per-step working set (SGNS state 4.8 GB, corpus ~55 MB) exceeds the 126 MB L2; "
               "the 88 MB CSR is L2-resident by design",
@@ -179,111 +179,172 @@ def make_graph():
     return g, V, ents
 
 
-# ------------------------------------------------------------ CPU oracle ----
-def cpu_sample(off, tgt, prd, roots_np, V, shards, batches: int, state=None):
-    """Oracle (numpy restatement of the reference) on a bounded sample.
+# ------------------------------------------------------- CPU reference ----
+REF_DIR = ROOT / "baseline" / "_ref"  # pip-installed, unmodified reference (git-ignored, travels to the box)
 
-    Walks: the given 8192-walk shards of the cfg2 corpus (walks.py:117-204);
-    SGNS: ``batches`` reference batches (23,933 pairs) drawn from those walks'
-    pairs, continuing ``state`` (init + RowAdam).  Returns timings + counts.
+
+def load_reference():
+    """The reference's walkvec package from baseline/_ref, or None if it was not installed."""
+    if not (REF_DIR / "walkvec" / "__init__.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import walkvec  # noqa: F401
+    import walkvec.w2v
+    import walkvec.walks
+
+    return walkvec
+
+
+class RefPipeline:
+    """The reference's own RDF2vec hot path, one replica (a _train_multi worker, w2v.py:579-746).
+
+    A step trains one block of the cfg2 work list end to end with the
+    reference's functions: ``walks._walk_shard`` over the block's walks
+    (walks.py:117-141, the block's shard stream SeedSequence([seed, 0, s])),
+    ``w2v.generate_pairs`` (:161-191), a fresh ``permutation`` of the block's
+    pairs, then every batch of 23,933 pairs (the 1 GiB rule at d 200) through
+    ``_draw_negatives`` -> ``_BatchData.batch_grads`` (= sgns_batch_grads) ->
+    ``apply_sparse_update`` (RowAdam) -- the loop body of _train_single
+    (:547-576).  Parameters and RowAdam state persist across steps.  With
+    the oracle port (``ref=None``) the same steps run oracle/ instead.
     """
-    from oracle import w2v as ow2v
-    from oracle import walks as owalks
 
-    if state is None:
-        inp, out = ow2v.init(V, DIM, SEED)
-        state = {"inp": inp, "out": out, "ai": ow2v.RowAdam(inp.shape, LR), "ao": ow2v.RowAdam(out.shape, LR),
-                 "rng": np.random.default_rng(np.random.SeedSequence([SEED, 1, 2, 0]))}
-    t0 = time.perf_counter()
-    pieces, lens = [], []
-    for s in shards:  # walks.py:168-173: shard s = work[8192 s : 8192 (s+1)] on SeedSequence([seed, 0, s])
-        w = np.arange(s * owalks.SHARD, min((s + 1) * owalks.SHARD, len(roots_np) * WALKS))
-        rows = owalks.walk_rows(off, tgt, prd, roots_np[w // WALKS], DEPTH, owalks._shard_rng(SEED, s, "pcg64"))
-        keep = rows != -1
-        pieces.append(rows[keep])
-        lens.append(keep.sum(axis=1))
-    tok = np.concatenate(pieces)
-    offs = np.concatenate([[0], np.cumsum(np.concatenate(lens))]).astype(np.int64)
-    t1 = time.perf_counter()
-    pr = ow2v.pairs(tok, offs, WINDOW)
-    t2 = time.perf_counter()
-    B = ow2v.batch_size(len(pr), DIM, NEG, BUDGET)
-    order = np.random.default_rng(np.random.SeedSequence([SEED, 1, 1])).permutation(len(pr))
-    t3 = time.perf_counter()
-    trained = 0
-    for b in range(batches):
-        idx = order[b * B:(b + 1) * B]
-        if len(idx) == 0:
-            break
-        negs = state["rng"].integers(0, V, size=len(idx) * NEG).reshape(len(idx), NEG)
-        loss, ir, ig, orr, og = ow2v.sgns_step(state["inp"], state["out"], pr[idx, 0], pr[idx, 1], negs)
-        ur, ug = ow2v.coalesce(ir, ig)
-        state["ai"].update(state["inp"], ur, ug)
-        ur, ug = ow2v.coalesce(orr, og)
-        state["ao"].update(state["out"], ur, ug)
-        trained += len(idx)
-    t4 = time.perf_counter()
-    hops = (len(tok) - (len(offs) - 1)) // 2
-    res = {"walk_s": t1 - t0, "pairs_s": t2 - t1, "shuffle_s": t3 - t2, "sgns_s": t4 - t3, "pairs_generated": len(pr),
-           "pairs_trained": trained, "hops": hops, "batch": B}
-    # pipeline seconds per trained pair: walk + pair generation scaled to the trained share, + SGNS
-    frac = trained / max(len(pr), 1)
-    res["pipeline_s"] = (res["walk_s"] + res["pairs_s"] + res["shuffle_s"]) * frac + res["sgns_s"]
-    res["pairs_per_s"] = trained / res["pipeline_s"]
-    res["hops_per_s"] = hops / res["walk_s"]
-    return res, state
+    def __init__(self, ref, graph, roots, V, wid):
+        self.ref, self.graph, self.roots, self.V = ref, graph, roots, V
+        self.B = 23_933
+        if ref is not None:
+            w2v = ref.w2v
+            self.cfg = w2v.TrainConfig(vector_size=DIM, window_size=WINDOW, negative_samples=NEG, learning_rate=LR,
+                                       min_count=0, epochs=1, batch_size=self.B)
+            self.model = w2v.init_embeddings(V, DIM, SEED)
+            self.model.touched_input = np.zeros(V, dtype=bool)
+            self.model.touched_output = np.zeros(V, dtype=bool)
+            self.opt_in = w2v.RowAdam(self.model.input_matrix.shape, LR)
+            self.opt_out = w2v.RowAdam(self.model.output_matrix.shape, LR)
+        else:
+            from oracle import w2v as ow2v
+
+            self.inp, self.out = ow2v.init(V, DIM, SEED)
+            self.opt_in, self.opt_out = ow2v.RowAdam(self.inp.shape, LR), ow2v.RowAdam(self.out.shape, LR)
+        self.candidates = np.arange(V)  # min_count 10 keeps every token at cfg2 (SURVEY §8d)
+        self.shuffle_rng = np.random.default_rng(np.random.SeedSequence([SEED, 1, 1, wid]))
+        self.neg_rng = np.random.default_rng(np.random.SeedSequence([SEED, 1, 2, wid]))
+        self.loss = None
+
+    def step(self, walk_begin: int, n_walks: int) -> dict:
+        t0 = time.perf_counter()
+        work = self.roots[(walk_begin + np.arange(n_walks)) // WALKS]
+        shard_rng = np.random.default_rng(np.random.SeedSequence([SEED, 0, walk_begin // 8192]))
+        if self.ref is not None:
+            tok, lens = self.ref.walks._walk_shard(self.graph, work, DEPTH, shard_rng)
+        else:
+            from oracle import walks as owalks
+
+            rows = owalks.walk_rows(*self.graph, work, DEPTH, shard_rng)
+            keep = rows != -1
+            tok, lens = rows[keep], keep.sum(axis=1)
+        offs = np.zeros(n_walks + 1, dtype=np.int64)
+        np.cumsum(lens, out=offs[1:])
+        t1 = time.perf_counter()
+        if self.ref is not None:
+            w2v = self.ref.w2v
+            pairs, _ = w2v.generate_pairs(w2v._Corpus(tok, offs), WINDOW, 0, self.V)
+            data = w2v._BatchData(w2v.SKIPGRAM, pairs=pairs)
+        else:
+            from oracle import w2v as ow2v
+
+            pairs = ow2v.pairs(tok, offs, WINDOW)
+        n = len(pairs)
+        order = self.shuffle_rng.permutation(n)
+        loss_sum = 0.0
+        for lo in range(0, n, self.B):
+            index = order[lo:lo + self.B]
+            if self.ref is not None:
+                negs = w2v._draw_negatives(data, self.cfg, self.neg_rng, self.candidates, len(index), self.V)
+                loss, ir, ig, orr, og = data.batch_grads(self.model, index, negs)
+                uin, uout = w2v.apply_sparse_update(self.model, ir, ig, orr, og, self.opt_in, self.opt_out)
+                self.model.touched_input[uin] = True
+                self.model.touched_output[uout] = True
+            else:
+                from oracle import w2v as ow2v
+
+                negs = self.candidates[self.neg_rng.integers(0, len(self.candidates), size=len(index) * NEG)]
+                sel = pairs[index]
+                loss, ir, ig, orr, og = ow2v.sgns_step(self.inp, self.out, sel[:, 0], sel[:, 1],
+                                                      negs.reshape(len(index), NEG))
+                self.opt_in.update(self.inp, *ow2v.coalesce(ir, ig))
+                self.opt_out.update(self.out, *ow2v.coalesce(orr, og))
+            loss_sum += loss * len(index)
+        t2 = time.perf_counter()
+        self.loss = loss_sum / n
+        hops = (len(tok) - n_walks) // 2
+        return {"s": t2 - t0, "walk_s": t1 - t0, "pairs": n, "hops": hops, "batches": -(-n // self.B)}
+
+
+def ref_graph(ref, off, tgt, prd, V):
+    """The reference's Graph (graph.py:31-41) over given CSR arrays, or the oracle's tuple."""
+    if ref is None:
+        return off, tgt, prd
+    return ref.graph.Graph(row_offsets=off, col_targets=tgt, col_predicates=prd, vertex_count=V)
 
 
 def host_csr(g):
     return g.row_offsets, g.col_targets, g.col_predicates
 
 
-# ------------------------------------------------------------- reference ----
-_REF = {}  # inherited by forked reference workers (CSR, roots, initial state)
+def _ref_kind(ref) -> str:
+    return "reference" if ref is not None else "port"
+
+
+_REF = {}  # inherited by forked reference workers (graph, roots)
 
 
 def _ref_worker(job):
-    """One reference worker: its own replica (init + RowAdam + negative stream, as a
-    _train_multi worker, w2v.py:579-746) over its own walk shards."""
-    wid, n_workers, warmup, steps, batches = job
-    from oracle import w2v as ow2v
-
-    inp, out = _REF["init"]  # forked: the replica's pages are copied on first write
-    state = {"inp": inp, "out": out, "ai": ow2v.RowAdam(inp.shape, LR), "ao": ow2v.RowAdam(out.shape, LR),
-             "rng": np.random.default_rng(np.random.SeedSequence([SEED, 1, 2, wid]))}
+    """One reference worker (own replica, own blocks); returns per-step timings."""
+    wid, n_workers, warmup, steps, walks_per_step = job
+    ref = load_reference() if _REF["use_ref"] else None
+    pipe = RefPipeline(ref, _REF["graph"], _REF["roots"], _REF["V"], wid)
+    total_walks = len(_REF["roots"]) * WALKS
     rows = []
     for i in range(warmup + steps):
-        shard = (i * n_workers + wid) % _REF["n_shards"]
-        res, state = cpu_sample(_REF["off"], _REF["tgt"], _REF["prd"], _REF["roots"], _REF["V"], [shard], batches, state)
+        blk = (i * n_workers + wid) * walks_per_step % total_walks
+        r = pipe.step(blk, min(walks_per_step, total_walks - blk))
         if i >= warmup:
-            rows.append((res["pipeline_s"], res["pairs_trained"], res["hops"], res["walk_s"]))
-    return rows
+            rows.append(r)
+    return rows, pipe.loss
+
+
+def ref_sample_text(cores, walks_per_step):
+    return (f"{cores} forked worker(s), one per host core, each a replica of the reference trainer (own parameters, "
+            f"RowAdam, negative stream, as a _train_multi worker) over its own blocks of the cfg2 work list; "
+            f"a step = {walks_per_step} walks of depth 8 (the reference's _walk_shard), generate_pairs, a permutation "
+            f"and every 23,933-pair batch over the block's pairs (sgns_batch_grads + apply_sparse_update, float64); "
+            f"value = pairs trained by all workers / the slowest worker's summed step time; the replica merge "
+            f"(every 64 batches in reproducible mode) is not reached within the run")
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference on all host cores (rank 0 only).
-
-    One forked worker per core, each a replica of the reference's multi-worker
-    trainer (own Adam state and negative stream, w2v.py:579-746) walking its own
-    8192-walk shards (walks.py:168-173) and training reference batches from them;
-    the replica merge every 64 batches (_merge_bundles) is not timed.  value =
-    pairs trained by all workers / the slowest worker's time.
-    """
+    """--impl reference: the reference's own CPU implementation on all host cores (rank 0 only)."""
     if rank != 0:
         return
     import multiprocessing as mp
 
-    import torch
+    from oracle import synth as osy
 
-    from oracle import w2v as ow2v
+    ref = load_reference()
+    # cfg2 input without the product library: the numpy restatement of the device generator
+    # (bit-identical graph, tests/test_gpu_synth.py), CSR by the reference's own build_graph
+    t0 = time.perf_counter()
+    edges, V, ents, _ = osy.barabasi_kg(N_ENT, M_BA, N_PRED, GEN_SEED)
+    if ref is not None:
+        graph = ref.graph.build_graph(edges, V)
+    else:
+        from oracle import walks as owalks
 
-    g, V, ents = make_graph()  # synthetic input only; the timed path below is pure numpy
-    off, tgt, prd = host_csr(g)
-    roots_np = ents.cpu().numpy()
-    del g
-    torch.cuda.empty_cache()
-    # one replica per core; each holds its own parameters + Adam state (~10.5 GB at cfg2 once its
-    # touched pages are copied), so the worker count is also capped by 60% of the available RAM
+        graph = owalks.csr(edges, V)
+    del edges
+    setup_s = time.perf_counter() - t0
     try:
         import psutil
 
@@ -291,30 +352,43 @@ def run_reference(args, rank, world):
     except ImportError:
         mem_cap = 8
     cores = int(args.ref_cores) if args.ref_cores else min(len(os.sched_getaffinity(0)), mem_cap)
-    _REF.update(off=off, tgt=tgt, prd=prd, roots=roots_np, V=V, n_shards=-(-len(roots_np) * WALKS // 8192),
-                init=ow2v.init(V, DIM, SEED))
-    jobs = [(w, cores, args.warmup, args.steps, args.ref_batches) for w in range(cores)]
+    _REF.update(graph=graph, roots=ents, V=V, use_ref=ref is not None)
+    jobs = [(w, cores, args.warmup, args.steps, args.ref_walks) for w in range(cores)]
     with mp.get_context("fork").Pool(cores) as pool:
         results = pool.map(_ref_worker, jobs)
-    per_worker_s = [sum(r[0] for r in rows) for rows in results]
-    trained = sum(r[1] for rows in results for r in rows)
-    hops = sum(r[2] for rows in results for r in rows)
-    walk_s = max(sum(r[3] for r in rows) for rows in results)
+    per_worker_s = [sum(r["s"] for r in rows) for rows, _ in results]
+    pairs = sum(r["pairs"] for rows, _ in results for r in rows)
+    hops = sum(r["hops"] for rows, _ in results for r in rows)
+    walk_s = max(sum(r["walk_s"] for r in rows) for rows, _ in results)
     tot = max(per_worker_s)
-    value = trained / tot
-    sample = (f"{cores} forked workers (one per host core), each per step: one 8192-walk shard of the cfg2 corpus "
-              f"(oracle walks) + {args.ref_batches} SGNS batches of 23,933 pairs from its pairs (oracle fp64 numpy, "
-              f"own replica as in _train_multi; merge not timed); walk/pair time scaled to the trained share; "
-              f"value = all pairs / slowest worker")
+    value = pairs / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args.roots),
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle/synth.py restatement of the device BA graph)",
+        "config": workload(args.roots, "fp64"),
         "walk_hops_per_s": hops / walk_s if walk_s else None,
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "port", "sample": sample},
+        "last_loss": results[0][1], "setup_s": setup_s,
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": _ref_kind(ref),
+                         "sample": ref_sample_text(cores, args.ref_walks)},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(args, off, tgt, prd, roots, V) -> dict:
+    """Our arm's cpu_baseline: the same reference pipeline on one core, a bounded sample."""
+    ref = load_reference()
+    pipe = RefPipeline(ref, ref_graph(ref, off, tgt, prd, V), roots, V, 0)
+    pipe.step(0, args.ref_walks)  # warm-up (page faults of the state)
+    rows = [pipe.step((i + 1) * args.ref_walks, args.ref_walks) for i in range(args.cpu_steps)]
+    tot = sum(r["s"] for r in rows)
+    pairs = sum(r["pairs"] for r in rows)
+    return {"value": pairs / tot, "unit": "pairs/s", "cores": 1, "kind": _ref_kind(ref),
+            "sample": ref_sample_text(1, args.ref_walks).replace("forked worker(s), one per host core", "process")
+            + f"; {args.cpu_steps} timed steps after 1 warm-up",
+            "walk_hops_per_s": sum(r["hops"] for r in rows) / sum(r["walk_s"] for r in rows),
+            "last_loss": pipe.loss}
 
 
 # ------------------------------------------------------------------- ours ---
@@ -334,7 +408,7 @@ def run_ours(args, rank, world, local):
     R = int(args.roots)
     n_blocks = -(-n_roots // R)
     cfg = wv.TrainConfig(vector_size=DIM, window_size=WINDOW, negative_samples=NEG, learning_rate=LR, epochs=1)
-    sess = wv.SkipGramSession(V, cfg, SEED, precision="fp32")
+    sess = wv.SkipGramSession(V, cfg, SEED, precision=args.precision)
     if world > 1:
         sess.attach_exchange(RankExchange())
     stream = torch.cuda.current_stream()
@@ -344,7 +418,7 @@ def run_ours(args, rank, world, local):
         b = (step * world + rank) % n_blocks
         return b * R, min((b + 1) * R, n_roots)
 
-    stats = {"walk_ms": [], "hops": 0, "walks": 0, "pairs": 0, "batches": 0, "sgns_ms": [], "phase_ms": {}}
+    stats = {"last_loss": None, "walk_ms": [], "hops": 0, "walks": 0, "pairs": 0, "batches": 0, "sgns_ms": [], "phase_ms": {}}
 
     def one_step(step, timed, profile=False):
         rb, re_ = block_range(step)
@@ -358,7 +432,8 @@ def run_ours(args, rank, world, local):
         e1.record(stream)
         n_w = (re_ - rb) * WALKS
         wc = wmod._compact(torch, dev, corpus, lengths, n_w, width, wmod.RANDOM)
-        sess.fit(wc, 1, profile=profile)
+        losses = sess.fit(wc, 1, profile=profile)
+        stats["last_loss"] = losses[-1]
         sess.sync()
         e2.record(stream)
         if timed:
@@ -447,7 +522,7 @@ def run_ours(args, rank, world, local):
         peak, peak_src = float(json.loads(peaks_path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     else:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    es = 4
+    es = 8 if args.precision == "fp64" else 4
     B = sess.last_batch_size
     n_batches = max(stats["batches"], 1)
     U = rows_per_batch_prof  # unique (row, matrix) updates per batch (profiled step)
@@ -510,20 +585,16 @@ def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         off, tgt, prd = host_csr(g)
-        res, _ = cpu_sample(off, tgt, prd, ents.cpu().numpy(), V, [0], args.ref_batches)
-        cpu = {"value": res["pairs_per_s"], "unit": "pairs/s", "cores": 1, "kind": "port",
-               "sample": f"oracle (numpy restatement, fp64): shard 0 of the cfg2 corpus (8192 walks, {res['hops']} hops, "
-                         f"{res['pairs_generated']} pairs) + {args.ref_batches} SGNS batches of {res['batch']} pairs; "
-                         f"walk+pair time scaled to the trained share",
-               "walk_hops_per_s": res["hops_per_s"], "sgns_pairs_per_s": res["pairs_trained"] / res["sgns_s"]}
+        cpu = cpu_baseline_leg(args, off, tgt, prd, ents.cpu().numpy(), V)
     walk_hops = sum_over_ranks(float(stats["hops"]), world, dev)
     walk_ms_tot = max_over_ranks(float(sum(stats["walk_ms"])), world, dev)
     sgns_ms_tot = max_over_ranks(float(sum(stats["sgns_ms"])), world, dev)
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "fp32", "data": "synthetic (device-generated BA graph, seed 7)",
-        "config": workload(R),
+        "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+        "data": "synthetic (device-generated BA graph, seed 7)",
+        "config": workload(R, args.precision),
         "walk_hops_per_s": walk_hops / (walk_ms_tot / 1e3),
         "sgns_pairs_per_s": total_pairs / (sgns_ms_tot / 1e3),
         "e2e_cfg2_epoch_s_extrapolated": (ms_max / args.steps) * n_blocks / world / 1e3,
@@ -535,7 +606,7 @@ def run_ours(args, rank, world, local):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "setup_s": setup_s,
-        "last_loss": None,
+        "last_loss": stats["last_loss"],  # epoch-mean SGNS loss of the last block (rank 0)
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -549,20 +620,25 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--roots", type=int, default=8192, help="entities per GPU per step")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--ref-batches", type=int, default=2, help="SGNS batches per CPU sample")
+    ap.add_argument("--ref-walks", type=int, default=384,
+                    help="walks per reference step (~48k pairs: two full 23,933-pair batches + a remainder)")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="timed steps of our arm's one-core cpu_baseline leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-cores", type=int, default=0, help="reference-arm workers (default: all host cores)")
+    ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64",
+                    help="parameter store (the reference computes in float64, w2v.py:127-130, 379-380)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        # CPU only: rank 0 runs the reference on the host cores, other ranks exit without work
+        run_reference(args, int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)))
+        return
     rank, world, local = dist_setup()
     if world != args.gpus and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     try:
-        if args.impl == "reference":
-            run_reference(args, rank, world)
-        else:
-            run_ours(args, rank, world, local)
+        run_ours(args, rank, world, local)
     finally:
         if world > 1:
             import torch.distributed as dist

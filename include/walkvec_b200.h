@@ -216,6 +216,13 @@ int wv_generate_pairs(const int32_t* tokens, const int64_t* offsets, int64_t n_w
 int64_t wv_candidates_workspace_bytes(int64_t vocab_size);
 int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, uint8_t* keep, int32_t* candidates,
                   int64_t* n_candidates, void* ws, int64_t ws_bytes, void* stream);
+/* inspection (skip-gram): decode the epoch's permuted positions [pos_begin,
+ * pos_begin + n) exactly as a batch does -> rows [n, 2 + negatives] (centre,
+ * context, negatives) and, if pair_index != NULL, the pair index each position
+ * maps to (native: the Feistel image in [0, n_pairs); explicit: perm[pos]).
+ * The pair-order and negative-distribution tests run through this. */
+int wv_sgns_decode(const WvSgnsBatch* batch, int64_t epoch, int64_t pos_begin, int64_t n, int32_t* rows,
+                   int64_t* pair_index, void* stream);
 /* reset the batch cursor to permuted position `start` (a worker's span start) */
 int wv_sgns_epoch_begin(WvSgnsDevState* state, int64_t epoch, int64_t start, void* stream);
 /* cbow_window = 0 for skip-gram, the CBOW window_size otherwise (2W context rows per item) */

@@ -38,12 +38,24 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
     lib = Path(out) if out else LIB
     if not force and out is None and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-o", str(lib) + ".tmp"]
-    cmd += [str(CSRC / s) for s in SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    # one nvcc per translation unit in parallel (sgns.cu dominates), then one link
+    objdir = ROOT / "build" / (lib.stem + "_obj")
+    objdir.mkdir(parents=True, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs = []
+    for s in SOURCES:
+        cmd = [_nvcc(), *compile_flags, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-c",
+               "-o", str(objdir / (s + ".o")), str(CSRC / s)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((s, subprocess.Popen(cmd)))
+    failed = [s for s, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {' '.join(failed)}")
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib) + ".tmp"]
+    link += [str(objdir / (s + ".o")) for s in SOURCES]
+    subprocess.run(link, check=True)
     os.replace(str(lib) + ".tmp", lib)
     return lib
 

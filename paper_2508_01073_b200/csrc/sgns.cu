@@ -415,6 +415,55 @@ __device__ __forceinline__ int32_t draw_negative(const CorpusDesc& D, int64_t po
   return D.negatives[pos * k + j];
 }
 
+// permuted position -> (centre, context): native mode walks Feistel position ->
+// length class -> walk -> window slot (the reference's shift-major pair order,
+// w2v.py:177-190); explicit mode reads pairs[perm[pos]].  ``q`` = the pair index.
+__device__ __forceinline__ int64_t decode_pair(const CorpusDesc& D, const Feistel& fs, int64_t pos, int32_t& center,
+                                               int32_t& context) {
+  if (D.mode == WV_PAIRS_NATIVE) {
+    const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, D.N);
+    int lo_c = 0, hi_c = D.n_classes;  // last class with start <= q
+    while (hi_c - lo_c > 1) {
+      int mid = (lo_c + hi_c) >> 1;
+      if (D.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
+    }
+    const int64_t L = D.class_len[lo_c];
+    const int64_t np = walk_pairs(L, D.window);
+    const int64_t r = q - D.class_pair_start[lo_c];
+    const int64_t wslot = r / np;
+    const int64_t local = r - wslot * np;
+    const int64_t walk = D.walks_by_class[D.class_walk_start[lo_c] + wslot];
+    int64_t cpos, xpos;
+    walk_pair_pos(L, D.window, local, cpos, xpos);
+    const int64_t base = D.offsets[walk];
+    center = D.tokens[base + cpos];
+    context = D.tokens[base + xpos];
+    return q;
+  }
+  const int64_t pi = D.perm[pos];
+  center = D.pairs[2 * pi];
+  context = D.pairs[2 * pi + 1];
+  return pi;
+}
+
+// test/inspection entry (wv_sgns_decode): positions [pos0, pos0 + n) of one
+// epoch -> rows [n, 2 + k] (centre, context, negatives) and the pair index q
+__global__ void sgns_decode_positions(CorpusDesc D, int k, int64_t epoch, int64_t pos0, int64_t n,
+                                      int32_t* __restrict__ rows, int64_t* __restrict__ qout) {
+  Feistel fs;
+  if (D.mode == WV_PAIRS_NATIVE) fs = make_feistel(D.seed, (uint64_t)epoch, D.N);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = pos0 + i;
+    int32_t c, x;
+    const int64_t q = decode_pair(D, fs, pos, c, x);
+    int32_t* row = rows + i * (2 + k);
+    row[0] = c;
+    row[1] = x;
+    for (int j = 0; j < k; ++j) row[2 + j] = draw_negative(D, pos, (uint64_t)epoch, j, k);
+    if (qout) qout[i] = q;
+  }
+}
+
 __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
   __shared__ CorpusDesc D;
   if (threadIdx.x == 0) D = *A.desc;
@@ -437,29 +486,7 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       const int64_t pos = lo + b;
       int32_t* row = A.idx + b * R;
       int32_t center, context;
-      if (D.mode == WV_PAIRS_NATIVE) {
-        const int64_t q = (int64_t)feistel_perm(fs, (uint64_t)pos, D.N);
-        int lo_c = 0, hi_c = D.n_classes;  // last class with start <= q
-        while (hi_c - lo_c > 1) {
-          int mid = (lo_c + hi_c) >> 1;
-          if (D.class_pair_start[mid] <= q) lo_c = mid; else hi_c = mid;
-        }
-        const int64_t L = D.class_len[lo_c];
-        const int64_t np = walk_pairs(L, D.window);
-        const int64_t r = q - D.class_pair_start[lo_c];
-        const int64_t wslot = r / np;
-        const int64_t local = r - wslot * np;
-        const int64_t walk = D.walks_by_class[D.class_walk_start[lo_c] + wslot];
-        int64_t cpos, xpos;
-        walk_pair_pos(L, D.window, local, cpos, xpos);
-        const int64_t base = D.offsets[walk];
-        center = D.tokens[base + cpos];
-        context = D.tokens[base + xpos];
-      } else {
-        const int64_t pi = D.perm[pos];
-        center = D.pairs[2 * pi];
-        context = D.pairs[2 * pi + 1];
-      }
+      decode_pair(D, fs, pos, center, context);
       row[0] = center;
       row[1] = context;
       group_claim(A, (uint32_t)center, b * R);
@@ -469,17 +496,7 @@ __global__ void __launch_bounds__(128) sgns_decode_kernel(PairArgs A) {
       const int64_t b = t / k;
       const int j = (int)(t - b * k);
       const int64_t pos = lo + b;
-      int32_t neg;
-      if (D.mode == WV_PAIRS_NATIVE) {
-        // Philox4x32 counter (position, epoch, j/2): two draws per call
-        uint32_t rnd[4] = {(uint32_t)pos, (uint32_t)((uint64_t)pos >> 32), (uint32_t)epoch, (uint32_t)(j >> 1)};
-        philox4x32_10(rnd, (uint32_t)D.seed ^ 0xA5A5F00Du, (uint32_t)(D.seed >> 32) ^ 0x3C6EF372u);
-        const uint64_t r64 = ((uint64_t)rnd[2 * (j & 1) + 1] << 32) | rnd[2 * (j & 1)];
-        const int64_t ci = (int64_t)mulhi64(r64, (uint64_t)D.n_candidates);
-        neg = D.candidates ? D.candidates[ci] : (int32_t)ci;
-      } else {
-        neg = D.negatives[pos * k + j];
-      }
+      const int32_t neg = draw_negative(D, pos, epoch, j, k);
       A.idx[b * R + 2 + j] = neg;
       group_claim(A, (uint32_t)(neg + A.V), b * R + 2 + j);
     }
@@ -3278,6 +3295,20 @@ int wv_candidates(const int64_t* freq, int64_t vocab_size, int64_t min_count, ui
   WV_LAUNCH_CHECK();
   WV_CUDA((excl_scan<uint8_t, int64_t>(keep, vocab_size, pos, n_candidates, scan_ws, st)));
   scatter_candidates<<<grid_for(vocab_size, 256), 256, 0, st>>>(keep, pos, vocab_size, candidates);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int wv_sgns_decode(const WvSgnsBatch* batch, int64_t epoch, int64_t pos_begin, int64_t n, int32_t* rows,
+                   int64_t* pair_index, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(batch != nullptr && rows != nullptr, "null argument");
+  WV_CHECK_ARG(batch->model == WV_MODEL_SKIPGRAM, "wv_sgns_decode: skip-gram batches only");
+  WV_CHECK_ARG(n >= 0 && pos_begin >= 0 && pos_begin + n <= batch->n_pairs, "positions out of range");
+  if (n == 0) return 0;
+  const CorpusDesc D = make_desc(batch);
+  sgns_decode_positions<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(D, batch->negatives, epoch, pos_begin, n,
+                                                                           rows, pair_index);
   WV_LAUNCH_CHECK();
   return 0;
 }

@@ -565,6 +565,18 @@ class _Trainer:
         if self.k > 0 and dc.n_candidates == 0:
             raise ValueError("no negative-sample candidates")
 
+    def decode(self, epoch: int, pos_begin: int = 0, n: int | None = None):
+        """Rows [n, 2+k] (centre, context, negatives) and pair indices [n] of the epoch's
+        permuted positions [pos_begin, pos_begin + n), decoded exactly as the batches
+        decode them (wv_sgns_decode; skip-gram)."""
+        torch = self.torch
+        n = self.N - int(pos_begin) if n is None else int(n)
+        rows = torch.empty((max(n, 1), 2 + self.k), dtype=torch.int32, device=self.dev)
+        q = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
+        _lib.call("wv_sgns_decode", C.byref(self.batch_struct), int(epoch), int(pos_begin), n, _lib.ptr(rows),
+                  _lib.ptr(q), _lib.stream_ptr())
+        return rows[:n], q[:n]
+
     def new_params(self):
         c = self.config
         return _Params(self.torch, self.dev, self.V, c.vector_size, self.seed, self.precision, c.use_sparse,

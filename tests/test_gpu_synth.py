@@ -129,3 +129,19 @@ def test_device_uniform_attachment_structure(wv):
     # E[distinct] = v (1 - (1 - 1/v)^m)
     expect = (v[1:] * (1 - (1 - 1 / v[1:]) ** m)).sum()
     assert abs(per.sum() - expect) / expect < 0.01
+
+
+@pytest.mark.parametrize("n,m,seed", [(2, 1, 7), (7, 3, 1), (50, 10, 7), (5000, 4, 3), (20000, 10, 7)])
+def test_barabasi_bit_exact_vs_oracle(wv, n, m, seed):
+    """csrc/synth.cu equals its numpy restatement (oracle/synth.py) edge for edge, and the
+    device encoding equals the oracle's first-occurrence encoding of the same triples."""
+    from oracle import synth as osy
+    from paper_2508_01073_b200 import synth
+
+    src, dst = synth.device_barabasi_edges(n, m, seed=seed)
+    osrc, odst = osy.barabasi_edges(n, m, seed)
+    assert np.array_equal(src.cpu().numpy(), osrc) and np.array_equal(dst.cpu().numpy(), odst)
+    e, V, ent, prd = synth.device_synthetic_kg("barabasi", n, m=m, predicates=12, seed=seed)
+    oe, oV, oent, oprd = osy.barabasi_kg(n, m, 12, seed)
+    assert V == oV and np.array_equal(e.cpu().numpy(), oe)
+    assert np.array_equal(ent.cpu().numpy(), oent) and np.array_equal(prd.cpu().numpy(), oprd)

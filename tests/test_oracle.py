@@ -148,3 +148,40 @@ def test_cbow_train_oracle_matches_reference(golden, name):
     np.testing.assert_allclose(r["losses"], g[f"{name}_losses"], rtol=1e-12)
     assert np.array_equal(r["touched_in"], g[f"{name}_touched_in"])
     assert np.array_equal(r["touched_out"], g[f"{name}_touched_out"])
+
+
+def test_synth_oracle_structure_and_encoding():
+    """oracle/synth.py: BA structure (benchgen.py:78-109 invariants) and the first-occurrence
+    encoding equal to the reference vocabulary fixture's rule (ingest.py:368-396)."""
+    from oracle import synth as osy
+
+    n, m = 3000, 6
+    src, dst = osy.barabasi_edges(n, m, 11)
+    v = np.arange(1, n)
+    assert np.array_equal(src, np.repeat(v, np.minimum(m, v)))
+    assert (dst < src).all() and (dst >= 0).all()
+    assert len(np.unique(src * n + dst)) == len(src)
+    assert osy.ba_edge_count(n, m) == len(src)
+    # in-degree + 1 attachment: old vertices collect far more edges than young ones
+    indeg = np.bincount(dst, minlength=n)
+    assert indeg[:30].mean() > 10 * indeg[-1000:].mean()
+    # encoding: tokens by first occurrence over (s, p, o), shared space, entity/predicate split
+    edges, V, ent, prd = osy.encode(np.array([5, 2, 5]), np.array([1, 0, 1]), np.array([2, 7, 7]), 10)
+    assert edges.tolist() == [[0, 1, 2], [2, 3, 4], [0, 1, 4]]
+    assert V == 5 and ent.tolist() == [0, 2, 4] and prd.tolist() == [1, 3]
+
+
+def test_synth_oracle_mulhi_and_philox():
+    from oracle import synth as osy
+
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 2**63, 1000, dtype=np.int64).astype(np.uint64) * np.uint64(2) + np.uint64(1)
+    b = rng.integers(0, 2**63, 1000, dtype=np.int64).astype(np.uint64)
+    got = osy.mulhi64(a, b)
+    want = [(int(x) * int(y)) >> 64 for x, y in zip(a, b)]
+    assert [int(x) for x in got] == want
+    # Philox4x32-10 known-answer vectors (Random123 kat_vectors: philox4x32 10 rounds)
+    c = osy.philox4x32_10([0], [0], [0], [0], 0, 0)
+    assert [int(x[0]) for x in c] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    c = osy.philox4x32_10([0xFFFFFFFF] * 1, [0xFFFFFFFF], [0xFFFFFFFF], [0xFFFFFFFF], 0xFFFFFFFF, 0xFFFFFFFF)
+    assert [int(x[0]) for x in c] == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
