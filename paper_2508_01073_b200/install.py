@@ -18,14 +18,16 @@ import importlib
 _saved: dict = {}
 
 
-def _wrap_train(train_fn):
+def _wrap_train(train_fn, precision: str, pairs: str):
     def train(corpus, vocab_size, config, rng_seed, on_event=None):
         from .w2v import TrainConfig
 
         cfg = TrainConfig(**{f: getattr(config, f) for f in TrainConfig.__dataclass_fields__})
-        model, losses = train_fn(corpus, vocab_size, cfg, rng_seed, on_event=on_event)
+        model, losses = train_fn(corpus, vocab_size, cfg, rng_seed, on_event=on_event, precision=precision,
+                                 pairs=pairs)
         return model, losses
 
+    train.__doc__ = f"walkvec.w2v.train on the B200 backend (precision={precision!r}, pairs={pairs!r})"
     return train
 
 
@@ -52,8 +54,20 @@ def _wrap_load_data(load_fn, pkg_name: str):
     return load_data
 
 
-def install(package: str = "walkvec"):
-    """Swap the reference's hot-path functions for the device implementations."""
+def install(package: str = "walkvec", *, precision: str = "fp64", pairs: str = "device"):
+    """Swap the reference's hot-path functions for the device implementations.
+
+    ``precision`` is the parameter store of the swapped ``train``: "fp64" (the
+    default: the reference's own arithmetic, w2v.py:127-130, 379-380) or "fp32"
+    (half the HBM bytes, tolerance-checked).  ``pairs`` is its pair/negative
+    source: "device" (Feistel permutation + Philox negatives, nothing
+    materialised on the host) or "numpy" (replays the reference's own numpy
+    streams: the same pairs, order and negatives as the reference's train()).
+    """
+    if precision not in ("fp64", "fp32"):
+        raise ValueError("precision must be 'fp64' or 'fp32'")
+    if pairs not in ("device", "numpy"):
+        raise ValueError("pairs must be 'device' or 'numpy'")
     from . import formats as dev_formats
     from . import walks as dev_walks
     from .pipeline import load_data as dev_load_data
@@ -68,9 +82,9 @@ def install(package: str = "walkvec"):
         (walks_mod, "bfs_walks", dev_walks.bfs_walks),
         (pkg, "random_walks", dev_walks.random_walks),
         (pkg, "bfs_walks", dev_walks.bfs_walks),
-        (w2v_mod, "train", _wrap_train(dev_train)),
-        (pipe_mod, "train", _wrap_train(dev_train)),
-        (pkg, "train", _wrap_train(dev_train)),
+        (w2v_mod, "train", _wrap_train(dev_train, precision, pairs)),
+        (pipe_mod, "train", _wrap_train(dev_train, precision, pairs)),
+        (pkg, "train", _wrap_train(dev_train, precision, pairs)),
         (pipe_mod, "load_data", _wrap_load_data(dev_load_data, package)),
         (pipe_mod, "save_embeddings_text", dev_formats.save_embeddings_text),
         (pipe_mod, "save_embeddings_tsv", dev_formats.save_embeddings_tsv),
@@ -79,7 +93,7 @@ def install(package: str = "walkvec"):
     ]
     try:
         cli_mod = importlib.import_module(f"{package}.cli")
-        targets.append((cli_mod, "train", _wrap_train(dev_train)))
+        targets.append((cli_mod, "train", _wrap_train(dev_train, precision, pairs)))
     except ImportError:
         pass
     for mod, name, fn in targets:
