@@ -391,6 +391,255 @@ def cpu_baseline_leg(args, off, tgt, prd, roots, V) -> dict:
             "last_loss": pipe.loss}
 
 
+
+# ------------------------------------------------- fp32 store, other configs --
+def fp32_leg(args, wv, wmod, g, ents, V, block_range, torch, dev):
+    """The fp32 parameter store beside the fp64 headline: throughput over the same
+    blocks, and its max |fp32 - fp64| after one block's epoch from the same init."""
+    cfg = wv.TrainConfig(vector_size=DIM, window_size=WINDOW, negative_samples=NEG, learning_rate=LR, epochs=1)
+
+    def block(step):
+        rb, re_ = block_range(step)
+        corpus, lengths, width = wmod.random_walks_fixed(g, ents, DEPTH, WALKS, SEED, "pcg64",
+                                                         work_begin=rb * WALKS, work_count=(re_ - rb) * WALKS)
+        n_w = (re_ - rb) * WALKS
+        return wmod._compact(torch, dev, corpus, lengths, n_w, width, wmod.RANDOM)
+
+    sess = wv.SkipGramSession(V, cfg, SEED, precision="fp32")
+    for i in range(args.warmup):
+        sess.fit(block(i), 1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pairs = 0
+    e0.record()
+    for i in range(args.fp32_steps):
+        sess.fit(block(args.warmup + i), 1)
+        pairs += sess.last_pairs
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    del sess
+    # deviation: one block's epoch (all its batches) in both stores from the same init and streams
+    wc = block(0)
+    s64 = wv.SkipGramSession(V, cfg, SEED, precision="fp64")
+    l64 = s64.fit(wc, 1)
+    s32 = wv.SkipGramSession(V, cfg, SEED, precision="fp32")
+    l32 = s32.fit(wc, 1)
+    dev_in = float((s64.params.inp - s32.params.inp.double()).abs().max())
+    dev_out = float((s64.params.out - s32.params.out.double()).abs().max())
+    mag = float(s64.params.inp.abs().max())
+    n_b = -(-s64.last_pairs // s64.last_batch_size)
+    del s64, s32
+    torch.cuda.empty_cache()
+    return {"value": pairs / (ms / 1e3), "unit": "pairs/s", "dtype": "f32", "steps": args.fp32_steps,
+            "ms_per_step": ms / args.fp32_steps,
+            "max_abs_dev_vs_fp64": max(dev_in, dev_out), "max_abs_param_fp64": mag,
+            "loss_fp64": l64[0], "loss_fp32": l32[0], "dev_batches": n_b,
+            "note": f"fp32 store (FMA, approximate sqrt/divide) vs the fp64 store after the {n_b} batches of one "
+                    f"block's epoch from the same init and device streams"}
+
+
+def _ref_train_sample(ref, corpus_ref, V, d, B, n_batches, min_count=10):
+    """Reference SGNS on the host: generate_pairs + n_batches batches of _train_single's loop body."""
+    w2v = ref.w2v
+    t0 = time.perf_counter()
+    pairs, freq = w2v.generate_pairs(corpus_ref, WINDOW, min_count, V)
+    t1 = time.perf_counter()
+    cfg = w2v.TrainConfig(vector_size=d, window_size=WINDOW, negative_samples=NEG, learning_rate=LR,
+                          min_count=min_count, epochs=1, batch_size=B)
+    model = w2v.init_embeddings(V, d, SEED)
+    opt_in, opt_out = w2v.RowAdam(model.input_matrix.shape, LR), w2v.RowAdam(model.output_matrix.shape, LR)
+    data = w2v._BatchData(w2v.SKIPGRAM, pairs=pairs)
+    cand = np.flatnonzero(freq >= min_count)
+    rng = np.random.default_rng(np.random.SeedSequence([SEED, 1, 2, 0]))
+    order = np.random.default_rng(np.random.SeedSequence([SEED, 1, 1])).permutation(len(pairs))
+    t2 = time.perf_counter()
+    for b in range(n_batches):
+        index = order[b * B:(b + 1) * B]
+        negs = w2v._draw_negatives(data, cfg, rng, cand, len(index), V)
+        _, ir, ig, orr, og = data.batch_grads(model, index, negs)
+        w2v.apply_sparse_update(model, ir, ig, orr, og, opt_in, opt_out)
+    t3 = time.perf_counter()
+    return {"pairs": len(pairs), "pairs_s": t1 - t0, "batch_s": (t3 - t2) / n_batches, "batches_timed": n_batches}
+
+
+def _ref_e2e_estimate(walk_s, tr, epochs, B):
+    """Reference seconds for the whole config from its measured pieces (walks, pair generation, per-batch time)."""
+    n_batches = -(-tr["pairs"] // B) * epochs
+    return walk_s + tr["pairs_s"] + n_batches * tr["batch_s"]
+
+
+def cfg_sgns_e2e(args, wv, synth, torch, name, gen, depth, number, d, epochs, ref):
+    """cfg1 / cfg4: device graph -> walks -> SGNS (fp64) -> vectors to the host, end to end."""
+    res = None
+    for rep in range(2):  # the first (one-epoch) pass pays one-time CUDA / graph-capture costs
+        run_epochs = epochs if rep else 1
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        edges, V, ents, _ = gen()
+        g = wv.build_graph(edges, V)
+        roots = ents.cpu().numpy()
+        corpus = wv.random_walks(g, roots, walk_depth=depth, walk_number=number, rng_seed=SEED)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        cfg = wv.TrainConfig(vector_size=d, window_size=WINDOW, negative_samples=NEG, learning_rate=LR,
+                             epochs=run_epochs, min_count=10)
+        model, losses = wv.train(corpus, V, cfg, SEED, precision=args.precision)
+        vec = model.input_matrix  # float64 host matrix (the EmbeddingTable's vectors)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        pairs = model.n_pairs * epochs
+        res = {"value": t2 - t0, "unit": "s", "higher_is_better": False, "dtype": "f64" if args.precision == "fp64"
+               else "f32", "graph_and_walks_s": t1 - t0, "train_and_export_s": t2 - t1,
+               "sgns_pairs_per_s": pairs / (t2 - t1), "pairs": pairs, "batch": model.batch_size,
+               "walks": len(corpus), "triples": g.edge_count, "vocab": V, "losses": losses,
+               "vectors": list(vec.shape)}
+    es = 8 if args.precision == "fp64" else 4
+    state_mb = 6 * res["vocab"] * d * es / 1e6
+    res["roofline"] = {"bound": "l2" if state_mb < 100 else "hbm", "unit": "GB/s",
+                       "achieved": res["sgns_pairs_per_s"] * 2 * (2 + NEG) * d * es / 1e9,
+                       "note": f"SGNS pair-phase algorithmic bytes (SURVEY §8d, 2(2+k)d·s per pair) / train time; "
+                               f"the parameter + Adam state is {state_mb:.0f} MB, "
+                               + ("L2-resident (126 MB L2): not an HBM-roofline case" if state_mb < 100 else "")}
+    if ref is not None and not args.no_cpu_baseline:
+        off, tgt, prd = g.row_offsets, g.col_targets, g.col_predicates
+        rgraph = ref_graph(ref, off, tgt, prd, V)
+        # bounded: the first 1/frac of the root list (walks + generate_pairs scale linearly with it)
+        frac = max(1, -(-len(roots) * number * (2 * depth + 1) // 20_000_000))
+        t0 = time.perf_counter()
+        rc = ref.walks.random_walks(rgraph, roots[: -(-len(roots) // frac)], walk_depth=depth, walk_number=number,
+                                    rng_seed=SEED)
+        walk_s = (time.perf_counter() - t0) * frac
+        tr = _ref_train_sample(ref, rc, V, d, res["batch"], 3)
+        tr["pairs"] = res["pairs"] // epochs
+        tr["pairs_s"] *= frac
+        est = _ref_e2e_estimate(walk_s, tr, epochs, res["batch"])
+        res["cpu_baseline"] = {"value": est, "unit": "s", "cores": 1, "kind": "reference",
+                               "sample": f"the reference's random_walks + generate_pairs over 1/{frac} of the "
+                                         f"{name} root list, scaled x{frac} ({walk_s:.2f} s + {tr['pairs_s']:.2f} s), "
+                                         f"and 3 timed "
+                                         f"batches of _train_single's loop ({tr['batch_s']:.2f} s each), "
+                                         f"value = walks + pairs + all {epochs} epoch(s) of batches at that rate "
+                                         f"(estimate; the reference's own init and export excluded)",
+                               "pairs_per_s": res["batch"] / tr["batch_s"]}
+    return res
+
+
+def cfg3_bfs(args, wv, torch, g, ents, ref):
+    """cfg3: BFS walks depth 4, at most 250 per entity, over every entity of the cfg2 graph."""
+    roots = ents.cpu().numpy()
+    R = 1 << 18
+    wv.bfs_walks(g, roots[:4096], 4, max_walks_per_root=250, with_table=False)  # warm-up
+    walks = tokens = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for rb in range(0, len(roots), R):
+        c, _ = wv.bfs_walks(g, roots[rb:rb + R], 4, max_walks_per_root=250, with_table=False)
+        walks += len(c)
+        tokens += c.total_tokens
+        del c
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    res = {"value": len(roots) / dt, "unit": "roots/s", "seconds": dt, "walks": walks, "tokens": tokens,
+           "walks_per_s": walks / dt,
+           "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": tokens * 4 / dt / 1e9,
+                        "note": "output bytes only (compacted int32 tokens): a lower bound of the traffic; "
+                                "the BFS frontier work (CSR reads, first-occurrence tables) is not counted"}}
+    if ref is not None and not args.no_cpu_baseline:
+        rgraph = ref_graph(ref, g.row_offsets, g.col_targets, g.col_predicates, g.vertex_count)
+        sample = roots[:: len(roots) // 100][:100]
+        t0 = time.perf_counter()
+        ref.walks.bfs_walks(rgraph, sample, 4)
+        rdt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": len(sample) / rdt, "unit": "roots/s", "cores": 1, "kind": "reference",
+                               "sample": "the reference's bfs_walks (uncapped: the cap is a prefix of its output "
+                                         "and saves it no work) on 100 uniformly spaced roots of the cfg2 graph"}
+    return res
+
+
+def cfg5_walks(args, wv, wmod, synth, torch, ref, peak):
+    """cfg5 walks on one GPU: BA(1e8, m=10), 200 predicates, depth 4 x 20 per entity (SGNS needs >= 4 GPUs)."""
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    edges, V, ents, _ = synth.device_synthetic_kg("barabasi", 100_000_000, m=10, predicates=200, seed=GEN_SEED)
+    g = wv.build_graph(edges, V)
+    del edges
+    torch.cuda.synchronize()
+    graph_s = time.perf_counter() - t0
+    n_roots = int(ents.numel())
+    R = 1 << 22
+    stream = torch.cuda.current_stream()
+    kern_ms, hops, walks = 0.0, 0, 0
+    t1 = time.perf_counter()
+    for rb in range(0, n_roots, R):
+        re_ = min(rb + R, n_roots)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(1_000_000)
+        e0.record(stream)
+        corpus, lengths, width = wmod.random_walks_fixed(g, ents, 4, 20, SEED, "pcg64", work_begin=rb * 20,
+                                                         work_count=(re_ - rb) * 20)
+        e1.record(stream)
+        e1.synchronize()
+        kern_ms += e0.elapsed_time(e1)
+        nw = (re_ - rb) * 20
+        hops += int((lengths[:nw].sum().item() - nw) // 2)
+        walks += nw
+        del corpus, lengths
+    wall = time.perf_counter() - t1
+    byt = 24 * hops + 8 * walks
+    res = {"value": hops / (kern_ms / 1e3), "unit": "hops/s", "graph_build_s": graph_s, "walks": walks,
+           "hops": hops, "walk_kernel_s": kern_ms / 1e3, "walks_wall_s": wall,
+           "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
+           "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": byt / (kern_ms * 1e-3) / 1e9, "peak": peak, "frac": byt / (kern_ms * 1e-3) / 1e9 / peak,
+                        "note": "SURVEY §8d walk bytes (24 B/hop + 8 B/walk) / summed walk-kernel time "
+                                "(CUDA events); CSR 8.8 GB: not L2-resident"},
+           "note": "cfg5's SGNS state (6 x 1e8 x 200 values) needs the row-sharded mode over >= 4 GPUs"}
+    if ref is not None and not args.no_cpu_baseline:
+        off = g.row_offsets
+        tgt, prd = g.col_targets, g.col_predicates
+        rgraph = ref_graph(ref, off, tgt, prd, V)
+        roots = ents[:2 * 8192 // 20 + 1].cpu().numpy()
+        work = np.repeat(roots, 20)[:2 * 8192]
+        t0 = time.perf_counter()
+        tok, lens = ref.walks._walk_shard(rgraph, work[:8192], 4, np.random.default_rng(
+            np.random.SeedSequence([SEED, 0, 0])))
+        tok2, lens2 = ref.walks._walk_shard(rgraph, work[8192:], 4, np.random.default_rng(
+            np.random.SeedSequence([SEED, 0, 1])))
+        rdt = time.perf_counter() - t0
+        rh = (len(tok) + len(tok2) - len(work)) // 2
+        res["cpu_baseline"] = {"value": rh / rdt, "unit": "hops/s", "cores": 1, "kind": "reference",
+                               "sample": "the reference's _walk_shard over the first two 8192-walk shards of the "
+                                         "cfg5 work list on the cfg5 CSR (host copy)"}
+        del off, tgt, prd, rgraph
+    del g, ents
+    torch.cuda.empty_cache()
+    return res
+
+
+def extra_configs(args, wv, wmod, synth, torch, g2, ents2, peak) -> dict:
+    """BASELINE.json configs 1, 3, 4, 5 on the driver's clock (rank 0, one GPU)."""
+    ref = load_reference() if not args.no_cpu_baseline else None
+    want = [c for c in args.configs.split(",") if c]
+    out = {}
+    if "cfg1" in want:
+        out["cfg1"] = cfg_sgns_e2e(args, wv, synth, torch, "cfg1", lambda: synth.device_synthetic_kg(
+            "barabasi", 10_000, m=5, predicates=20, seed=GEN_SEED), 4, 10, 100, 1, ref)
+        out["cfg1"]["workload"] = ("cfg1: BA(10k, m=5), 20 predicates; walks depth 4 x 10; SGNS d100 w5 k5, 1 epoch; "
+                                   "end to end (graph, walks, training, float64 vectors on the host)")
+    if "cfg3" in want:
+        out["cfg3"] = cfg3_bfs(args, wv, torch, g2, ents2, ref)
+        out["cfg3"]["workload"] = "cfg3: BFS walks depth 4, <= 250 per entity, all 1M entities of the cfg2 graph"
+    if "cfg4" in want:
+        out["cfg4"] = cfg_sgns_e2e(args, wv, synth, torch, "cfg4", lambda: synth.device_synthetic_kg(
+            "erdos_renyi", 15_000, p=0.001378, predicates=237, seed=GEN_SEED), 16, 500, 100, args.cfg4_epochs, ref)
+        out["cfg4"]["workload"] = (f"cfg4: ER(15k, p=0.001378), 237 predicates (~310k triples); walks depth 16 x 500; "
+                                   f"SGNS d100 w5 k5, {args.cfg4_epochs} epochs; end to end")
+    if "cfg5" in want:
+        out["cfg5_walks"] = cfg5_walks(args, wv, wmod, synth, torch, ref, peak)
+        out["cfg5_walks"]["workload"] = "cfg5: BA(1e8, m=10) -> ~1e9 triples, 200 predicates; walks depth 4 x 20"
+    return out
+
 # ------------------------------------------------------------------- ours ---
 def run_ours(args, rank, world, local):
     import torch
@@ -530,7 +779,11 @@ def run_ours(args, rank, world, local):
     walk_bytes = 24 * stats["hops"] / args.steps + 8 * stats["walks"] / args.steps
     ph = {k_: float(np.mean(v_)) for k_, v_ in stats["phase_ms"].items()}
     pair_bytes = (2 + NEG) * DIM * es * B  # gathers of the 2+k rows (SURVEY §8d pair phase, first half)
-    owner_bytes = (2 + NEG) * DIM * es * B + 8 * DIM * es * U  # scatter half + RowAdam rows
+    # the update phase's required DRAM bytes: RowAdam read-modify-write of p, m, v for each unique
+    # row (this design keeps no gradient accumulator, so §8d's g read + zeroing is not moved) + one
+    # read of the batch's U/G rows the contributions come from
+    owner_bytes = 6 * DIM * es * U + 2 * DIM * es * B
+    owner_bytes_8d = (2 + NEG) * DIM * es * B + 8 * DIM * es * U  # scatter half + 8 d s per row
     per = n_batches / args.steps
     kern = {
         "walk": {"ms": walk_ms, "bytes": walk_bytes, "per_step": 1},
@@ -547,6 +800,7 @@ def run_ours(args, rank, world, local):
         v_["frac"] = v_["gbs"] / peak if v_["gbs"] else None
     dom = max((k_ for k_ in kern if kern[k_]["bytes"]), key=lambda k_: kern[k_]["share_of_step"])
     batch_bytes = pair_bytes + owner_bytes
+    frac_8d = owner_bytes_8d / (kern["sgns_owner_adam(flat light rows + heavy pieces)"]["ms"] * 1e-3) / 1e9 / peak
     batch_ms = ph.get("batch", float("nan"))
     # ncu DRAM traffic per launch of the owner phase's kernels (same batch geometry), newest capture
     traffic, traffic_src, batch_traffic = None, None, None
@@ -564,7 +818,7 @@ def run_ours(args, rank, world, local):
             kern["walk"]["ncu_l2_hit_rate_pct"] = t_["random_walk_kernel"].get("l2_hit_rate_pct")
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
-        "frac": kern[dom]["frac"], "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+        "frac": kern[dom]["frac"], "frac_survey_8d_bytes": frac_8d, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
         "algorithmic_bytes_per_launch": kern[dom]["bytes"], "avg_launch_ms": kern[dom]["ms"],
         "kernels": kern,
         "sgns_batch": {"bytes": batch_bytes, "ms": batch_ms, "gbs": batch_bytes / (batch_ms * 1e-3) / 1e9,
@@ -576,7 +830,10 @@ def run_ours(args, rank, world, local):
         # the same kernel against its measured DRAM bytes (the algorithmic figure counts a row
         # gathered by the pair phase and then updated by the Adam phase twice)
         "frac_of_measured_traffic": (traffic / (kern[dom]["ms"] * 1e-3) / 1e9 / peak if traffic else None),
-        "note": "achieved = SURVEY §8d algorithmic bytes per launch / mean CUDA-event launch time. walk: events "
+        "note": "achieved = required bytes per launch / mean CUDA-event launch time; update phase: 6 d s per unique "
+                "row (p, m, v read + write) + 2 B d s (the U/G rows read once); gather: (2+k) d s per pair; "
+                "frac_survey_8d_bytes uses SURVEY §8d's figure (8 d s per row + (2+k) d s per pair), which counts "
+                "a gradient accumulator this design does not have. walk: events "
                 "around the walk kernel in the timed steps; SGNS phases: CUDA events around the phases of every 16th "
                 "batch of one extra step right after the timed region, run eagerly (event nodes inside CUDA graphs "
                 "would distort the graph-replayed timing). traffic: see profiles/",
@@ -586,6 +843,14 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         off, tgt, prd = host_csr(g)
         cpu = cpu_baseline_leg(args, off, tgt, prd, ents.cpu().numpy(), V)
+    fp32 = None
+    if args.precision == "fp64" and args.fp32_steps > 0:
+        fp32 = fp32_leg(args, wv, wmod, g, ents, V, block_range, torch, dev)
+    configs = None
+    if rank == 0 and world == 1 and args.configs:
+        from paper_2508_01073_b200 import synth
+
+        configs = extra_configs(args, wv, wmod, synth, torch, g, ents, peak)
     walk_hops = sum_over_ranks(float(stats["hops"]), world, dev)
     walk_ms_tot = max_over_ranks(float(sum(stats["walk_ms"])), world, dev)
     sgns_ms_tot = max_over_ranks(float(sum(stats["sgns_ms"])), world, dev)
@@ -607,6 +872,8 @@ def run_ours(args, rank, world, local):
         "clocks": clocks.summary(),
         "setup_s": setup_s,
         "last_loss": stats["last_loss"],  # epoch-mean SGNS loss of the last block (rank 0)
+        "fp32_store": fp32,
+        "configs": configs,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -623,6 +890,10 @@ def main():
     ap.add_argument("--ref-walks", type=int, default=384,
                     help="walks per reference step (~48k pairs: two full 23,933-pair batches + a remainder)")
     ap.add_argument("--cpu-steps", type=int, default=3, help="timed steps of our arm's one-core cpu_baseline leg")
+    ap.add_argument("--fp32-steps", type=int, default=3, help="timed steps of the fp32-store leg (0: skip)")
+    ap.add_argument("--configs", default="cfg1,cfg3,cfg4,cfg5",
+                    help="other BASELINE configs timed after the headline (rank 0, N=1; '' to skip)")
+    ap.add_argument("--cfg4-epochs", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-cores", type=int, default=0, help="reference-arm workers (default: all host cores)")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64",

@@ -18,13 +18,18 @@ import importlib
 _saved: dict = {}
 
 
-def _wrap_train(train_fn, precision: str, pairs: str):
+def _wrap_train(train_fn, precision: str, pairs: str, package: str):
     def train(corpus, vocab_size, config, rng_seed, on_event=None):
-        from .w2v import TrainConfig
+        from .w2v import TrainConfig, TrainingDiverged
 
         cfg = TrainConfig(**{f: getattr(config, f) for f in TrainConfig.__dataclass_fields__})
-        model, losses = train_fn(corpus, vocab_size, cfg, rng_seed, on_event=on_event, precision=precision,
-                                 pairs=pairs)
+        try:
+            model, losses = train_fn(corpus, vocab_size, cfg, rng_seed, on_event=on_event, precision=precision,
+                                     pairs=pairs)
+        except TrainingDiverged as err:
+            # the caller catches the reference's own type (w2v.py:46-52; pipeline.py wraps it in PipelineError)
+            ref_type = importlib.import_module(f"{package}.w2v").TrainingDiverged
+            raise ref_type(err.epoch, err.batch) from err
         return model, losses
 
     train.__doc__ = f"walkvec.w2v.train on the B200 backend (precision={precision!r}, pairs={pairs!r})"
@@ -82,9 +87,9 @@ def install(package: str = "walkvec", *, precision: str = "fp64", pairs: str = "
         (walks_mod, "bfs_walks", dev_walks.bfs_walks),
         (pkg, "random_walks", dev_walks.random_walks),
         (pkg, "bfs_walks", dev_walks.bfs_walks),
-        (w2v_mod, "train", _wrap_train(dev_train, precision, pairs)),
-        (pipe_mod, "train", _wrap_train(dev_train, precision, pairs)),
-        (pkg, "train", _wrap_train(dev_train, precision, pairs)),
+        (w2v_mod, "train", _wrap_train(dev_train, precision, pairs, package)),
+        (pipe_mod, "train", _wrap_train(dev_train, precision, pairs, package)),
+        (pkg, "train", _wrap_train(dev_train, precision, pairs, package)),
         (pipe_mod, "load_data", _wrap_load_data(dev_load_data, package)),
         (pipe_mod, "save_embeddings_text", dev_formats.save_embeddings_text),
         (pipe_mod, "save_embeddings_tsv", dev_formats.save_embeddings_tsv),
@@ -93,7 +98,7 @@ def install(package: str = "walkvec", *, precision: str = "fp64", pairs: str = "
     ]
     try:
         cli_mod = importlib.import_module(f"{package}.cli")
-        targets.append((cli_mod, "train", _wrap_train(dev_train, precision, pairs)))
+        targets.append((cli_mod, "train", _wrap_train(dev_train, precision, pairs, package)))
     except ImportError:
         pass
     for mod, name, fn in targets:
