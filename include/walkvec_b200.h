@@ -267,6 +267,13 @@ int wv_shard_requests(const WvSgnsModel* model, const WvSgnsBatch* batch, void* 
                       int64_t vocab_global, int nshard, int shard, int64_t item_begin, int64_t n_items,
                       uint32_t* cursor, int64_t* keys, int32_t* items, int32_t* ident, int64_t* counts,
                       void* stream);
+/* split sizes of a skip-gram batch's request all-to-all, computed without
+ * communication: decodes positions [pos_begin, pos_begin + rows) of `epoch`
+ * (into scratch_rows [rows, 2 + negatives]) and counts counts[s * nshard + o]
+ * = rows requested by rank s (its pair share) from owner o.  Run one batch
+ * ahead with an async copy, it removes the host round trip per batch. */
+int wv_shard_count_requests(const WvSgnsBatch* batch, int64_t epoch, int64_t pos_begin, int64_t rows, int nshard,
+                            int32_t* scratch_rows, int64_t* counts, void* stream);
 int wv_shard_serve(const WvSgnsModel* model, const int64_t* keys, int64_t n, int64_t vocab_global, int nshard,
                    void* rows, void* stream);
 int wv_shard_place(const void* rows, const int32_t* items, int64_t n, int vector_size, int precision,

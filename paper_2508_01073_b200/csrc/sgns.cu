@@ -2697,6 +2697,28 @@ __global__ void shard_requests(const int32_t* __restrict__ idx, int64_t item_beg
   }
 }
 
+// requests of a skip-gram batch per (requesting rank, owning rank), from decoded
+// rows [rows, R]: pair b belongs to requester b / bl (shard.py's pair shares),
+// each of its R rows to owner row % nshard.  Lets every rank know every split
+// size of the batch's all-to-alls without exchanging counts (shard lookahead).
+__global__ void shard_count_matrix(const int32_t* __restrict__ rows_idx, int64_t rows, int R, int64_t bl,
+                                   int nshard, unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int local[64 * 64];
+  const int nn = nshard * nshard;
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) local[i] = 0;
+  __syncthreads();
+  const int64_t n = rows * R;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = rows_idx[i];
+    if (t < 0) continue;
+    const int s = (int)((i / R) / bl);
+    atomicAdd(local + s * nshard + (int)((uint32_t)t % (uint32_t)nshard), 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nn; i += blockDim.x)
+    if (local[i]) atomicAdd(counts + i, (unsigned long long)local[i]);
+}
+
 __global__ void shard_offsets(uint32_t* cursor, int nshard, int64_t* counts) {
   // cursor[0..n) holds counts after pass 0: copy them out, turn the cursor into offsets
   uint32_t run = 0;
@@ -3812,6 +3834,24 @@ int wv_shard_requests(const WvSgnsModel* model, const WvSgnsBatch* batch, void* 
                                                            vocab_global, nshard, 1, cursor, keys, items, ident);
     WV_LAUNCH_CHECK();
   }
+  return 0;
+}
+
+int wv_shard_count_requests(const WvSgnsBatch* batch, int64_t epoch, int64_t pos_begin, int64_t rows, int nshard,
+                            int32_t* scratch_rows, int64_t* counts, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(nshard >= 1 && nshard <= 64, "nshard must be in [1, 64]");
+  WV_CHECK_ARG(batch != nullptr && batch->model == WV_MODEL_SKIPGRAM, "skip-gram batches only");
+  cudaStream_t st = (cudaStream_t)stream;
+  WV_CUDA(cudaMemsetAsync(counts, 0, (size_t)nshard * nshard * 8, st));
+  if (rows <= 0) return 0;
+  const int rc = wv_sgns_decode(batch, epoch, pos_begin, rows, scratch_rows, nullptr, stream);
+  if (rc) return rc;
+  const int R = 2 + batch->negatives;
+  const int64_t bl = (rows + nshard - 1) / nshard;
+  shard_count_matrix<<<grid_for(rows * R, 256, 148 * 2), 256, 0, st>>>(scratch_rows, rows, R, bl, nshard,
+                                                                     (unsigned long long*)counts);
+  WV_LAUNCH_CHECK();
   return 0;
 }
 

@@ -43,9 +43,75 @@ class RankExchange:
         self.rank = dist.get_rank(group)
         self.world_size = dist.get_world_size(group)
 
+    @property
+    def _staged(self) -> bool:
+        # gloo (multi-process tests on one GPU / CPU): collectives on host copies
+        return self.dist.get_backend(self.group) != "nccl"
+
+    def _all_reduce(self, t, op=None):
+        op = op if op is not None else self.dist.ReduceOp.SUM
+        if self._staged and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+    def _all_gather(self, out, local):
+        if self._staged and local.is_cuda:
+            parts = list(out.cpu().chunk(self.world_size))
+            self.dist.all_gather(parts, local.cpu().contiguous(), group=self.group)
+            import torch
+
+            out.copy_(torch.cat(parts))
+        else:
+            self.dist.all_gather_into_tensor(out, local.contiguous(), group=self.group)
+
     def all_reduce_(self, *tensors):
         for t in tensors:
-            self.dist.all_reduce(t, group=self.group)
+            self._all_reduce(t)
+
+    def merge_deltas_(self, deltas, counts, dim: int, sparse_fraction: float = 0.5):
+        """Sum per-row deltas ([V*d] each) and touch counts ([V] each) across ranks, in place.
+
+        A rank's delta is non-zero only on the rows it touched this round
+        (count > 0 before the reduction).  When every rank touched few rows
+        (world * max touched < sparse_fraction * V) only those rows travel:
+        their ids and rows are all-gathered and summed in rank order (the same
+        order on every rank, so all replicas stay identical); otherwise one
+        dense all-reduce per matrix.  Returns "sparse" or "dense".
+        """
+        import torch
+
+        V = int(counts[0].numel())
+        touched = [torch.nonzero(c > 0).flatten() for c in counts]
+        nmax = torch.tensor([max(int(t.numel()) for t in touched)], dtype=torch.int64, device=counts[0].device)
+        self._all_reduce(nmax, self.dist.ReduceOp.MAX)
+        n = int(nmax.item())
+        for c in counts:
+            self._all_reduce(c)
+        if self.world_size * n >= sparse_fraction * V:
+            for dlt in deltas:
+                self._all_reduce(dlt)
+            return "dense"
+        W = self.world_size
+        for dlt, rows in zip(deltas, touched):
+            dv = dlt.view(V, dim)
+            ids = torch.full((n,), -1, dtype=torch.int64, device=dlt.device)
+            ids[: rows.numel()] = rows
+            vals = torch.zeros((n, dim), dtype=dlt.dtype, device=dlt.device)
+            vals[: rows.numel()] = dv[rows]
+            all_ids = torch.empty((W * n,), dtype=torch.int64, device=dlt.device)
+            all_vals = torch.empty((W * n, dim), dtype=dlt.dtype, device=dlt.device)
+            self._all_gather(all_ids, ids)
+            self._all_gather(all_vals, vals)
+            dv.zero_()
+            for r in range(W):  # rank order: a row's ids are unique within one rank
+                ir = all_ids[r * n:(r + 1) * n]
+                ok = ir >= 0
+                dv.index_put_((ir[ok],), all_vals[r * n:(r + 1) * n][ok], accumulate=True)
+        return "sparse"
 
     def reduce_epoch(self, loss_sum: float, count: int, diverged):
         import torch

@@ -26,6 +26,7 @@ index is replicated (every rank decodes every pair).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -139,23 +140,54 @@ def train_row_sharded(corpus, vocab_size: int, config, rng_seed: int, exchange: 
     if pairs == "numpy":
         shuffle_rng = np.random.default_rng(np.random.SeedSequence([tr.seed, 1, 1]))
         neg_rng = np.random.default_rng(np.random.SeedSequence([tr.seed, 1, 2, 0]))
+    # skip-gram: every split size of a batch's all-to-alls is computed on the device one batch
+    # ahead (wv_shard_count_requests) and copied to pinned host memory asynchronously, so no
+    # batch waits on a device -> host round trip; CBOW reads its counts synchronously
+    lookahead = tr.cbow_window == 0 and not os.environ.get("WV_SHARD_SYNC_COUNTS")
+    check = bool(os.environ.get("WV_SHARD_CHECK"))
+    if lookahead:
+        scratch = torch.empty(max(B * R, 1), dtype=torch.int32, device=dev)
+        cnt_dev = torch.empty(N * N, dtype=torch.int64, device=dev)
+        cnt_host = [torch.empty(N * N, dtype=torch.int64, pin_memory=torch.cuda.is_available()) for _ in range(2)]
+        cnt_evt = [torch.cuda.Event() for _ in range(2)]
+
+    def issue_counts(epoch, lo, slot):
+        _lib.call("wv_shard_count_requests", C.byref(bs), epoch, lo, min(B, Npairs - lo), N, _lib.ptr(scratch),
+                  _lib.ptr(cnt_dev), st)
+        cnt_host[slot].copy_(cnt_dev, non_blocking=True)
+        cnt_evt[slot].record()
+
     losses = []
     for epoch in range(config.epochs):
         if pairs == "numpy":
             order = shuffle_rng.permutation(Npairs)
             tr._upload_epoch_streams(order, [(lo, min(B, Npairs - lo), neg_rng) for lo in range(0, Npairs, B)])
         _lib.call("wv_sgns_epoch_begin", _lib.ptr(p.state), epoch, 0, st)
-        for lo in range(0, Npairs, B):
+        starts = list(range(0, Npairs, B))
+        if lookahead:
+            issue_counts(epoch, 0, 0)
+        for bi, lo in enumerate(starts):
             rows = min(B, Npairs - lo)
             bs.batch_rows = rows
             _lib.call("wv_shard_decode_group", model, C.byref(bs), _lib.ptr(ws), ws.numel(), V, N, r, st)
+            if lookahead and bi + 1 < len(starts):
+                issue_counts(epoch, starts[bi + 1], (bi + 1) % 2)
             bl = -(-rows // N)
             pb = min(r * bl, rows)
             pc = min(rows, pb + bl) - pb
             _lib.call("wv_shard_requests", model, C.byref(bs), _lib.ptr(ws), ws.numel(), V, N, r, pb * R, pc * R,
                       _lib.ptr(cursor), _lib.ptr(keys), _lib.ptr(items), _lib.ptr(ident), _lib.ptr(counts), st)
-            send_counts = counts.cpu().tolist()
-            recv_counts = ex.exchange_counts(counts)
+            if lookahead:
+                cnt_evt[bi % 2].synchronize()  # recorded a batch ago: already complete
+                M = cnt_host[bi % 2].view(N, N).tolist()
+                send_counts = M[r]
+                recv_counts = [M[s_][r] for s_ in range(N)]
+                if check:
+                    assert send_counts == counts.cpu().tolist(), (send_counts, counts.cpu().tolist())
+                    assert recv_counts == ex.exchange_counts(counts), "request counts differ across ranks"
+            else:
+                send_counts = counts.cpu().tolist()
+                recv_counts = ex.exchange_counts(counts)
             req = ex.all_to_all(keys, send_counts, recv_counts)
             served = torch.empty((max(len(req), 1), d), dtype=dt, device=dev)
             _lib.call("wv_shard_serve", model, _lib.ptr(req), len(req), V, N, _lib.ptr(served), st)

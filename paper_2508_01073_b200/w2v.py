@@ -692,7 +692,8 @@ class _Trainer:
                     touched_in.zero_()
                     touched_out.zero_()
                 if exchange is not None:
-                    exchange.all_reduce_(delta_sum_in, delta_sum_out, cnt_in, cnt_out)
+                    self.last_merge = exchange.merge_deltas_((delta_sum_in, delta_sum_out), (cnt_in, cnt_out),
+                                                             c.vector_size)
                 # every replica applies the same merge -> identical union rows
                 for i, r in enumerate(reps):
                     last = i == len(reps) - 1
@@ -804,7 +805,8 @@ class SkipGramSession:
         p.touched_out |= self._round_out
         self._round_in.zero_()
         self._round_out.zero_()
-        self.exchange.all_reduce_(self._delta_in, self._delta_out, self._cnt_in, self._cnt_out)
+        self.last_merge = self.exchange.merge_deltas_((self._delta_in, self._delta_out),
+                                                      (self._cnt_in, self._cnt_out), self.config.vector_size)
         _lib.call("wv_replica_apply", _lib.ptr(p.inp), _lib.ptr(self._snap_in), _lib.ptr(self._delta_in),
                   _lib.ptr(self._cnt_in), self.V, self.config.vector_size, p.precision, st)
         _lib.call("wv_replica_apply", _lib.ptr(p.out), _lib.ptr(self._snap_out), _lib.ptr(self._delta_out),

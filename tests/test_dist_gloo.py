@@ -104,3 +104,42 @@ def _exchange_worker(rank, world):
 
 def test_replica_exchange_matches_reference_merge():
     _run(2, _exchange_worker)
+
+
+def _merge_worker(rank, world, V, d, frac_rows):
+    """merge_deltas_: the sparse (touched rows only) and dense paths give the reference merge."""
+    ex = RankExchange()
+    results = {}
+    for mode, frac in (("sparse", 0.99), ("dense", 1e-9)):
+        rng = np.random.default_rng(100 + rank)
+        touched = np.zeros(V, dtype=bool)
+        touched[rng.choice(V, int(frac_rows * V), replace=False)] = True
+        touched[0] = True  # a row every rank touches
+        delta = np.zeros((V, d))
+        delta[touched] = rng.normal(size=(touched.sum(), d))
+        dl = torch.from_numpy(delta.ravel().copy())
+        cnt = torch.from_numpy(touched.astype(np.float32))
+        got = ex.merge_deltas_((dl,), (cnt,), d, sparse_fraction=frac)
+        assert got == mode, (got, mode)
+        results[mode] = (dl.numpy().reshape(V, d).copy(), cnt.numpy().copy())
+        # expected: sum over ranks of their deltas, counts summed
+        exp_d = np.zeros((V, d))
+        exp_c = np.zeros(V, dtype=np.float32)
+        for r in range(world):
+            rr = np.random.default_rng(100 + r)
+            t = np.zeros(V, dtype=bool)
+            t[rr.choice(V, int(frac_rows * V), replace=False)] = True
+            t[0] = True
+            dd = np.zeros((V, d))
+            dd[t] = rr.normal(size=(t.sum(), d))
+            exp_d = exp_d + dd
+            exp_c += t
+        np.testing.assert_allclose(results[mode][0], exp_d, rtol=0, atol=1e-12)
+        assert np.array_equal(results[mode][1], exp_c)
+    if world == 2:  # two addends: both paths are exact and identical
+        assert np.array_equal(results["sparse"][0], results["dense"][0])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sparse_touched_row_merge(world):
+    _run(world, _merge_worker, 50, 4, 0.1)

@@ -30,6 +30,7 @@ def _worker(rank, world, port, case, out_dir):
     import torch.distributed as dist
 
     torch.cuda.set_device(0)
+    os.environ["WV_SHARD_CHECK"] = "1"  # lookahead split sizes == the exchanged device counts, every batch
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     import paper_2508_01073_b200 as wv
     from paper_2508_01073_b200.shard import train_row_sharded
