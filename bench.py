@@ -847,7 +847,7 @@ def run_ours(args, rank, world, local):
     if args.precision == "fp64" and args.fp32_steps > 0:
         fp32 = fp32_leg(args, wv, wmod, g, ents, V, block_range, torch, dev)
     configs = None
-    if rank == 0 and world == 1 and args.configs:
+    if rank == 0 and world == 1 and args.configs not in ("", "none"):
         from paper_2508_01073_b200 import synth
 
         configs = extra_configs(args, wv, wmod, synth, torch, g, ents, peak)

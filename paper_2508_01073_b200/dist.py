@@ -135,3 +135,43 @@ class RankExchange:
 
 def env_rank() -> tuple[int, int, int]:
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def bfs_walks_rank(graph, start_vertices=None, walk_depth: int = 5, *, max_walks_per_root: int | None = None,
+                   rank: int | None = None, world: int | None = None, group=None):
+    """BFS walks of this rank's contiguous root range with GLOBAL walk ids (BFS row).
+
+    Roots are independent (walks.py:261-310: each root's walks depend on that
+    root only), so rank r walks ``rank_slice(len(roots), r, world)`` with no
+    communication; the one exchange is an all-gather of the ranks' walk counts,
+    whose exclusive prefix is this rank's first global walk id.  The
+    PathTable's walk ids are shifted by it, so concatenating the ranks'
+    outputs in rank order gives exactly the single-process
+    ``bfs_walks(graph, roots, walk_depth)``.  Returns (corpus, table, first_walk_id).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .walks import _resolve_roots, as_device_graph, bfs_walks
+
+    if rank is None or world is None:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    g = as_device_graph(graph)
+    roots = _resolve_roots(g, start_vertices)
+    rb, re_ = rank_slice(len(roots), rank, world)
+    if re_ > rb:
+        corpus, table = bfs_walks(g, roots[rb:re_], walk_depth, max_walks_per_root=max_walks_per_root)
+        n = len(corpus)
+    else:
+        corpus, table, n = None, None, 0
+    counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(counts, torch.tensor([n], dtype=torch.int64), group=group)
+    else:
+        counts[0][0] = n
+    base = int(sum(int(c.item()) for c in counts[:rank]))
+    if table is not None:
+        table.walk_ids = table.walk_ids + base
+    if corpus is not None:
+        corpus.first_walk_id = base
+    return corpus, table, base

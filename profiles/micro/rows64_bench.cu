@@ -18,14 +18,26 @@
 constexpr int D = 200;
 constexpr int C2 = D / 2;  // 100 double2 chunks per row
 
+template <bool FAST>
 __device__ __forceinline__ void adam2(double2& p, double2& m, double2& v, double2 g, double r1, double r2, double lr) {
   auto one = [&](double& pp, double& mm, double& vv, double gg) {
-    mm = 0.9 * mm + 0.1 * gg;
-    vv = 0.999 * vv + 0.001 * gg * gg;
-    pp = pp - lr * (mm / r1) / (sqrt(vv / r2) + 1e-8);
+    mm = __dadd_rn(__dmul_rn(0.9, mm), __dmul_rn(0.1, gg));
+    vv = __dadd_rn(__dmul_rn(0.999, vv), __dmul_rn(__dmul_rn(0.001, gg), gg));
+    if (FAST)  // per-row reciprocals of the bias corrections, one division
+      pp = pp - __ddiv_rn(lr * (mm * r1), __dsqrt_rn(vv * r2) + 1e-8);
+    else       // numpy's order: three correctly rounded divisions + sqrt
+      pp = pp - __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mm, r1)), __dadd_rn(__dsqrt_rn(__ddiv_rn(vv, r2)), 1e-8));
   };
   one(p.x, m.x, v.x, g.x);
   one(p.y, m.y, v.y, g.y);
+}
+
+__global__ void k_fill(double* a, int64_t n, double lo, double hi, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+    a[i] = lo + (hi - lo) * (double)(x >> 11) * (1.0 / 9007199254740992.0);
+  }
 }
 
 // flat (row, chunk) space; pstride = elements between rows; moff = offset of m from p, voff of v
@@ -59,7 +71,12 @@ __global__ void __launch_bounds__(256) k_flat(const uint32_t* __restrict__ rows,
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (o[u] >= 0) {
-        adam2(p[u], m[u], v[u], g[u], 1.1, 1.2, lr);
+        if (mode == 4) {  // bandwidth only: trivial math
+          p[u].x += g[u].x; p[u].y += g[u].y; m[u].x += g[u].x; m[u].y += g[u].y; v[u].x += g[u].x; v[u].y += g[u].y;
+        } else if (mode == 3)
+          adam2<true>(p[u], m[u], v[u], g[u], 1.0 / 0.1, 1.0 / 0.001, lr);
+        else
+          adam2<false>(p[u], m[u], v[u], g[u], 0.1, 0.001, lr);
         if (mode == 1) {  // read-only: keep the result alive without storing rows
           if (p[u].x == 12345.0) *(double2*)(P + o[u]) = p[u];
         } else {
@@ -83,9 +100,14 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&F, 256 << 20));
   CK(cudaMalloc(&rows, n * 4));
   CK(cudaMalloc(&rows_sorted, n * 4));
-  CK(cudaMemset(S, 0, 3 * NE * 8));
-  CK(cudaMemset(I, 0, 3 * NE * 8));
-  CK(cudaMemset(G, 0, (int64_t)n * D * 8));
+  // realistic magnitudes (zeros would send sqrt / division down their special-case paths)
+  for (double* base : {S, I}) {
+    k_fill<<<1184, 256>>>(base, NE, -0.01, 0.01, 1);
+    k_fill<<<1184, 256>>>(base + NE, NE, -1e-5, 1e-5, 2);
+    k_fill<<<1184, 256>>>(base + 2 * NE, NE, 1e-13, 1e-10, 3);
+  }
+  k_fill<<<1184, 256>>>(G, (int64_t)n * D, -1e-5, 1e-5, 4);
+  CK(cudaDeviceSynchronize());
   std::vector<uint32_t> all(V);
   for (int64_t i = 0; i < V; ++i) all[i] = (uint32_t)i;
   std::mt19937_64 rng(1);
@@ -141,6 +163,12 @@ int main(int argc, char** argv) {
       [&]() { k_flat<2><<<148 * 16, 256>>>(rows, n, S, D, NE, 2 * NE, G, 0.01, 2); }, wo);
   run("inter random read-only g2368", [&]() { k_flat<2><<<148 * 16, 256>>>(rows, n, I, 3 * D, D, 2 * D, G, 0.01, 1); },
       ro);
+  run("separate random FAST-math g2368", [&]() { k_flat<2><<<148 * 16, 256>>>(rows, n, S, D, NE, 2 * NE, G, 0.01, 3); },
+      rw);
+  run("separate random NO-math g2368", [&]() { k_flat<2><<<148 * 16, 256>>>(rows, n, S, D, NE, 2 * NE, G, 0.01, 4); },
+      rw);
+  run("separate random NO-math u1 g4736", [&]() { k_flat<1><<<148 * 32, 256>>>(rows, n, S, D, NE, 2 * NE, G, 0.01, 4); },
+      rw);
   run("memcpy 1 GB d2d", [&]() { CK(cudaMemcpyAsync(I, S, 1 << 30, cudaMemcpyDeviceToDevice)); }, 2.0 * (1 << 30));
   return 0;
 }

@@ -120,3 +120,52 @@ def test_two_rank_training_and_session_merge(tmp_path, sparse_fraction, expect):
         expect_p[hit] = snap.reshape(V, d)[hit] + dsum[hit] / cnt[hit, None]
         for x in (a, b):
             assert np.array_equal(x[f"post_{side}"].reshape(V, d), expect_p), side
+
+
+def _bfs_worker(rank, world, port, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    import paper_2508_01073_b200 as wv
+    from paper_2508_01073_b200.dist import bfs_walks_rank
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("barabasi", 3000, m=4, predicates=8, seed=9)
+    graph = wv.build_graph(edges, V)
+    corpus, table, base = bfs_walks_rank(graph, ents[::7], 3, max_walks_per_root=40)
+    np.savez(os.path.join(out_dir, f"bfs_rank{rank}.npz"), tokens=corpus.tokens, offsets=corpus.offsets,
+             src=table.sources, dst=table.targets, wid=table.walk_ids, base=np.array(base))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bfs_root_ranges_with_global_walk_ids(tmp_path, world):
+    """Rank-sharded BFS (root ranges, walk ids by an exclusive scan of the ranks' counts)
+    concatenates to the single-process bfs_walks corpus and PathTable."""
+    import torch.multiprocessing as mp
+
+    import paper_2508_01073_b200 as wv
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    mp.start_processes(_bfs_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    edges, V, ents, _ = synthetic_kg("barabasi", 3000, m=4, predicates=8, seed=9)
+    graph = wv.build_graph(edges, V)
+    corpus, table = wv.bfs_walks(graph, ents[::7], 3, max_walks_per_root=40)
+    parts = [np.load(tmp_path / f"bfs_rank{r}.npz") for r in range(world)]
+    toks = np.concatenate([p["tokens"] for p in parts])
+    offs = [np.zeros(1, dtype=np.int64)]
+    for p in parts:
+        offs.append(p["offsets"][1:] + offs[-1][-1])
+    assert np.array_equal(toks, corpus.tokens) and np.array_equal(np.concatenate(offs), corpus.offsets)
+    assert np.array_equal(np.concatenate([p["src"] for p in parts]), table.sources)
+    assert np.array_equal(np.concatenate([p["dst"] for p in parts]), table.targets)
+    assert np.array_equal(np.concatenate([p["wid"] for p in parts]), table.walk_ids)
+    assert [int(p["base"]) for p in parts] == [int(sum(len(q["offsets"]) - 1 for q in parts[:r])) for r in
+                                               range(world)]
