@@ -622,6 +622,9 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 #ifndef WV_GATHER_WARPS
 #define WV_GATHER_WARPS 8
 #endif
+#ifndef WV_GATHER_PREFETCH
+#define WV_GATHER_PREFETCH 0  // pairs (per warp, in ring steps) whose rows are L2-prefetched ahead of their copies
+#endif
 #ifndef WV_GATHER_STAGES
 #define WV_GATHER_STAGES 3  // 3 x 8 warps: one 134 KB CTA per SM leaves room for the side stream (+2.7 % vs 2 x 8)
 #endif
@@ -698,6 +701,15 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
       issue(nb, (it + kBulkStages - 1) % kBulkStages, r_next);
     }
     r_next = row_of(nb + stride);
+    if constexpr (WV_GATHER_PREFETCH > 0) {
+      // L2 prefetch of a pair further ahead: more bytes in flight than the ring's shared memory holds
+      const int64_t pf = nb + (int64_t)WV_GATHER_PREFETCH * stride;
+      const int32_t rp = row_of(pf);
+      if (rp >= 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((lane < ctxw ? in : out) + (int64_t)rp * d),
+                     "r"(row_bytes)
+                     : "memory");
+    }
     while (!mbar_try_wait(mybar + stage, (phase >> stage) & 1u)) {
     }
     phase ^= 1u << stage;
@@ -3583,7 +3595,8 @@ struct LaunchPieces {
 
 // owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
 // then (split mode) the Adam pass and (dense mode) the dense Adam sweep
-static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t st) {
+static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t st, int t_light = -1,
+                          int t_heavy = -1) {
   const WvSgnsModel* model = c.model;
   const int64_t V = c.V, items = c.items;
   const int d = c.d;
@@ -3595,8 +3608,10 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
     WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
     int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, ss->h);
     if (rc) return rc;
+    if (t_heavy >= 0) WV_STAMP(t_heavy, ss->h);
     rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
     if (rc) return rc;
+    if (t_light >= 0) WV_STAMP(t_light, st);
     WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
     WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
     return 0;
@@ -3719,11 +3734,12 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
   WV_CUDA(side_stream(&ss));
   WV_CUDA(cudaEventRecord(ss->fork, st));
   WV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
-  // optional timeline (profiling): per batch i, slots timer_base + 5i + {0 side start,
-  // 1 side end, 2 gather start, 3 gather end, 4 update end}
+  // optional timeline (profiling): per batch i, slots timer_base + 7i + {0 side start,
+  // 1 side end, 2 gather start, 3 gather end, 4 update end, 5 light-row owner end,
+  // 6 heavy pieces end}
   for (int64_t i = 0; i < count; ++i) {
     const int h = (int)(i & 1);
-    const int t0 = 5 * (int)i;
+    const int t0 = 7 * (int)i;
     if (i >= 2) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[h], 0));
     WV_STAMP(t0 + 0, ss->s);
     WV_CUDA_RC(enqueue_decode(c, h, ss->s));
@@ -3736,7 +3752,7 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
     WV_CUDA_RC(enqueue_gather(c, h, st));
     WV_STAMP(t0 + 3, st);
     WV_CUDA(cudaStreamWaitEvent(st, ss->grp[h], 0));
-    WV_CUDA_RC(enqueue_update(c, h, ss, st));
+    WV_CUDA_RC(enqueue_update(c, h, ss, st, c.timer ? t0 + 5 : -1, c.timer ? t0 + 6 : -1));
     WV_STAMP(t0 + 4, st);
     WV_CUDA(cudaEventRecord(ss->own[h], st));
   }

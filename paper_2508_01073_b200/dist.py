@@ -76,27 +76,29 @@ class RankExchange:
         """Sum per-row deltas ([V*d] each) and touch counts ([V] each) across ranks, in place.
 
         A rank's delta is non-zero only on the rows it touched this round
-        (count > 0 before the reduction).  When every rank touched few rows
-        (world * max touched < sparse_fraction * V) only those rows travel:
-        their ids and rows are all-gathered and summed in rank order (the same
-        order on every rank, so all replicas stay identical); otherwise one
-        dense all-reduce per matrix.  Returns "sparse" or "dense".
+        (count > 0 before the reduction).  Per matrix: when every rank touched
+        few rows (world * max touched < sparse_fraction * V) only those rows
+        travel -- their ids and rows are all-gathered and summed in rank order
+        (the same order on every rank, so all replicas stay identical);
+        otherwise one dense all-reduce.  Returns the path per matrix, e.g.
+        "sparse,dense".
         """
         import torch
 
         V = int(counts[0].numel())
         touched = [torch.nonzero(c > 0).flatten() for c in counts]
-        nmax = torch.tensor([max(int(t.numel()) for t in touched)], dtype=torch.int64, device=counts[0].device)
+        nmax = torch.tensor([int(t.numel()) for t in touched], dtype=torch.int64, device=counts[0].device)
         self._all_reduce(nmax, self.dist.ReduceOp.MAX)
-        n = int(nmax.item())
+        nmax = nmax.tolist()
         for c in counts:
             self._all_reduce(c)
-        if self.world_size * n >= sparse_fraction * V:
-            for dlt in deltas:
-                self._all_reduce(dlt)
-            return "dense"
         W = self.world_size
-        for dlt, rows in zip(deltas, touched):
+        modes = []
+        for dlt, rows, n in zip(deltas, touched, nmax):
+            if W * n >= sparse_fraction * V:
+                self._all_reduce(dlt)
+                modes.append("dense")
+                continue
             dv = dlt.view(V, dim)
             ids = torch.full((n,), -1, dtype=torch.int64, device=dlt.device)
             ids[: rows.numel()] = rows
@@ -111,7 +113,8 @@ class RankExchange:
                 ir = all_ids[r * n:(r + 1) * n]
                 ok = ir >= 0
                 dv.index_put_((ir[ok],), all_vals[r * n:(r + 1) * n][ok], accumulate=True)
-        return "sparse"
+            modes.append("sparse")
+        return ",".join(modes)
 
     def reduce_epoch(self, loss_sum: float, count: int, diverged):
         import torch

@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B/n on one box: one short bench per library variant (WV_LIB), twice each.
 #   LIBS="path1 path2 ..." bash profiles/abn.sh
-ARGS=${ARGS:-"--steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline"}
+ARGS=${ARGS:-"--steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline --configs none --fp32-steps 0"}
 for i in 1 2; do
   for L in $LIBS; do
     n=$(basename $L .so)

@@ -120,7 +120,7 @@ def _merge_worker(rank, world, V, d, frac_rows):
         dl = torch.from_numpy(delta.ravel().copy())
         cnt = torch.from_numpy(touched.astype(np.float32))
         got = ex.merge_deltas_((dl,), (cnt,), d, sparse_fraction=frac)
-        assert got == mode, (got, mode)
+        assert got == mode, (got, mode)  # one matrix: one path
         results[mode] = (dl.numpy().reshape(V, d).copy(), cnt.numpy().copy())
         # expected: sum over ranks of their deltas, counts summed
         exp_d = np.zeros((V, d))

@@ -34,9 +34,9 @@ def _free_port():
 def _corpus(wv, seed):
     from paper_2508_01073_b200.synth import synthetic_kg
 
-    edges, V, ents, _ = synthetic_kg("barabasi", 1500, m=4, predicates=10, seed=3)
+    edges, V, ents, _ = synthetic_kg("barabasi", 6000, m=4, predicates=10, seed=3)
     graph = wv.build_graph(edges, V)
-    return wv.random_walks(graph, ents, walk_depth=4, walk_number=3, rng_seed=seed), V
+    return wv.random_walks(graph, ents[::4], walk_depth=4, walk_number=3, rng_seed=seed), V
 
 
 CFG = dict(min_count=1, vector_size=24, epochs=2, window_size=3, negative_samples=4, batch_size=256, workers=2,
@@ -68,7 +68,7 @@ def _worker(rank, world, port, out_dir, sparse_fraction):
     sess.attach_exchange(ex)
     orig = ex.merge_deltas_
     ex.merge_deltas_ = lambda d, c, dim: orig(d, c, dim, sparse_fraction=sparse_fraction)
-    small = wv.WalkCorpus(*_first_walks(_corpus(wv, 20 + rank)[0], 60 if rank == 0 else 90))
+    small = wv.WalkCorpus(*_first_walks(_corpus(wv, 20 + rank)[0], 8 if rank == 0 else 12))
     snap_in = sess.params.inp.double().cpu().numpy().copy()
     snap_out = sess.params.out.double().cpu().numpy().copy()
     sess.fit(small, 1)
@@ -89,7 +89,7 @@ def _first_walks(corpus, n):
     return corpus.tokens[: off[-1]], off
 
 
-@pytest.mark.parametrize("sparse_fraction,expect", [(0.99, "sparse"), (1e-9, "dense")])
+@pytest.mark.parametrize("sparse_fraction,expect", [(0.99, "sparse,sparse"), (1e-9, "dense,dense")])
 def test_two_rank_training_and_session_merge(tmp_path, sparse_fraction, expect):
     import torch.multiprocessing as mp
 
