@@ -343,6 +343,7 @@ struct PairArgs {
   int shard;
   int64_t Vl;     // local rows per matrix (key space of the claims: [0, 2 Vl))
   uint32_t* rank; // [items] an item's position among its row's items (from the claim)
+  uint8_t* flag;  // [2V] row keys the batch touches (the split owner of the previous batch reads them)
 };
 
 // ------------------------------------------------------------ grouping ---
@@ -359,7 +360,7 @@ struct PairArgs {
 // The list order inside a row is arbitrary; the owner kernels restore slot
 // order (warp ranking / CTA radix sort) before summing, so results are
 // deterministic, and reset cnt[key] to 0 for the next batch.
-enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3, GC_PIECES = 4 };
+enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3, GC_PIECES = 4, GC_NA = 5, GC_NB = 6 };
 
 // global row key (row, or V + row) -> local key of this rank, false if another rank owns it
 __device__ __forceinline__ bool owned_key(uint32_t key, int64_t V, int nshard, int shard, int64_t Vl, uint32_t& lk) {
@@ -385,6 +386,7 @@ __device__ __forceinline__ void group_claim(const PairArgs& A, uint32_t key, int
     const uint32_t r = atomicAdd(A.cnt + lk, 1u);
     A.rank[item] = r;
     first = r == 0u;
+    if (first && A.flag) A.flag[lk] = 1;
   }
   // new rows take unique ids with one atomic per warp (GC_UNIQUE is one address)
   const uint32_t fm = __ballot_sync(active, first);
@@ -1343,6 +1345,9 @@ struct OwnerArgs {
   const Segment* segs;
   const Segment* heavy;
   const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
+  const uint32_t* seg_base;   // split owner: the launch's segments start at segs + *seg_base (null: 0)
+  int bookkeep;               // 1: this launch advances the batch counters (one launch per batch)
+  uint8_t* flag;              // row-key membership flags of this batch, cleared per row (null: none)
   const void* U;
   const void* G;
   const void* coef;
@@ -1802,9 +1807,10 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
   const int d = A.d;
   const uint32_t C = (uint32_t)(d / EPC);
   const uint32_t nseg = *A.seg_count;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  const Segment* segs = A.segs + (A.seg_base ? *A.seg_base : 0u);
+  if (A.bookkeep && blockIdx.x == 0 && threadIdx.x == 0) {
     WvSgnsDevState* st = A.state;
-    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)(nseg + A.gctr[GC_HEAVY]));
+    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)(A.gctr[GC_LIGHT] + A.gctr[GC_HEAVY]));
     st->batch += 1;
     st->step += 1;
   }
@@ -1845,7 +1851,7 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
     auto issue = [&](uint32_t i, int s) {
       uint32_t r;
       const int32_t c = chunk_of(i, r);
-      const Segment sg = A.segs[r];
+      const Segment sg = segs[r];
       sbuf[s][tid] = sg;
       const bool so = sg.key >= (uint32_t)A.V;
       const int64_t row = so ? (int64_t)sg.key - A.V : (int64_t)sg.key;
@@ -1909,6 +1915,7 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
       if (c == 0) {
         (side_out ? A.touched_out : A.touched_in)[row] = 1;
         A.cnt[sg.key] = 0;
+        if (A.flag) A.flag[sg.key] = 0;
       }
       s ^= 1;
     }
@@ -1932,7 +1939,7 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
           c2 -= (int32_t)C;
         }
         if (c2 == 0 || (threadIdx.x & 31) == 0) {
-          const uint32_t key = A.segs[r2].key;
+          const uint32_t key = segs[r2].key;
           const bool so = key >= (uint32_t)A.V;
           const int64_t row = so ? (int64_t)key - A.V : (int64_t)key;
           const uint32_t bytes = (uint32_t)(d * sizeof(T));
@@ -1961,7 +1968,7 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
         ++r;
         cr[u] -= (int32_t)C;
       }
-      if (ok[u]) sg[u] = A.segs[r];
+      if (ok[u]) sg[u] = segs[r];
     }
     Chunk<T, EPC> p[kFlatU], m[kFlatU], vv[kFlatU], g[kFlatU];
 #pragma unroll
@@ -2017,6 +2024,7 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
       if (cr[u] == 0) {
         (side_out ? A.touched_out : A.touched_in)[row] = 1;
         A.cnt[sg[u].key] = 0;
+        if (A.flag) A.flag[sg[u].key] = 0;
       }
     }
   }
@@ -2095,6 +2103,12 @@ template <typename T, int EPC, int MAXC>
 #endif
 #ifndef WV_HEAVY_GRID
 #define WV_HEAVY_GRID (148 * 4)
+#endif
+#ifndef WV_SPLIT_B_PER_SM
+#define WV_SPLIT_B_PER_SM 2  // split owner: B-row CTAs per SM (they share the SMs with the next gather)
+#endif
+#ifndef WV_SPLIT_OWNER
+#define WV_SPLIT_OWNER 1  // pipelined batches: apply the next batch's rows first, the rest beside its gather
 #endif
 #ifndef WV_OWNER_PER_SM
 #define WV_OWNER_PER_SM 4  // light-row owner CTAs per SM (room for the concurrent heavy pieces); 0: all resident
@@ -2429,6 +2443,7 @@ __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc
       (side_out ? A.touched_out : A.touched_in)[row] = 1;
       if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
       A.cnt[sg.key] = 0;
+      if (A.flag) A.flag[sg.key] = 0;
     }
   }
 }
@@ -2924,9 +2939,10 @@ struct LaunchPair {
 // from and joins back into the caller's stream through these events.
 struct SideStream {
   int dev = -1;
-  cudaStream_t s = nullptr, h = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr, fork_h = nullptr, join_h = nullptr;
+  cudaStream_t s = nullptr, h = nullptr, b = nullptr;  // b: the split owner's B rows
+  cudaEvent_t fork = nullptr, join = nullptr, fork_h = nullptr, join_h = nullptr, fork_b = nullptr;
   cudaEvent_t dec[2] = {nullptr, nullptr}, grp[2] = {nullptr, nullptr}, own[2] = {nullptr, nullptr};
+  cudaEvent_t bdone[2] = {nullptr, nullptr};
 };
 
 static cudaError_t side_stream(SideStream** out) {
@@ -2951,8 +2967,9 @@ static cudaError_t side_stream(SideStream** out) {
       e = cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, WV_SIDE_PRIO ? hi_prio : lo_prio);
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&ss.h, cudaStreamNonBlocking, WV_HEAVY_PRIO ? hi_prio : lo_prio);
-    cudaEvent_t* evs[] = {&ss.fork, &ss.join, &ss.fork_h, &ss.join_h, &ss.dec[0], &ss.dec[1],
-                          &ss.grp[0], &ss.grp[1], &ss.own[0], &ss.own[1]};
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ss.b, cudaStreamNonBlocking, lo_prio);
+    cudaEvent_t* evs[] = {&ss.fork, &ss.join, &ss.fork_h, &ss.join_h, &ss.fork_b, &ss.dec[0], &ss.dec[1],
+                          &ss.grp[0], &ss.grp[1], &ss.own[0], &ss.own[1], &ss.bdone[0], &ss.bdone[1]};
     for (cudaEvent_t* ev : evs)
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
@@ -2982,13 +2999,15 @@ struct BatchHalf {
   void* partial;     // [max_pieces, d] piece partial sums
   uint32_t* rowdone; // per heavy row: pieces finished (zero between batches)
   uint32_t* rank;    // [items] claim rank of each item within its row
+  uint8_t* flag;     // [2V] 1 for every row key this half's batch touches (set by decode, cleared by the owner)
+  Segment* segs2;    // light segments regrouped: rows the next batch also touches first (split owner)
 };
 
 struct BatchWs {
   CorpusDesc* desc;
-  void* U;
-  void* G;
-  void* coef;
+  void* U[2];  // per half: batch i's update reads half i&1 while batch i+1's gather writes the other
+  void* G[2];
+  void* coef[2];
   double* partials;
   void* gsum;
   BatchHalf half[2];
@@ -3011,9 +3030,12 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int R, int64_
   // depend on B, so a short final batch sees the same ones
   w.desc = (CorpusDesc*)take(sizeof(CorpusDesc));
   for (int h = 0; h < 2; ++h) w.half[h].cnt = (uint32_t*)take(2 * V * 4);
-  w.U = take(B * d * es);
-  w.G = take(B * d * es);
-  w.coef = take(B * (k + 1) * es);
+  for (int h = 0; h < 2; ++h) w.half[h].flag = (uint8_t*)take(2 * V);
+  for (int h = 0; h < 2; ++h) {
+    w.U[h] = take(B * d * es);
+    w.G[h] = take(B * d * es);
+    w.coef[h] = take(B * (k + 1) * es);
+  }
   w.partials = (double*)take(148 * 32 * 8);
   w.gsum = split_adam_requested() ? take(items * d * es) : nullptr;
   for (int h = 0; h < 2; ++h) {
@@ -3030,6 +3052,7 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int R, int64_
     x.partial = take(max_pieces(items) * d * es);
     x.rowdone = (uint32_t*)take((items / (kLightMax + 1) + 1) * 4);  // zeroed per batch with gctr
     x.rank = (uint32_t*)take(items * 4);
+    x.segs2 = (Segment*)take(items * (int64_t)sizeof(Segment));
   }
   return off + 1024;
 }
@@ -3105,6 +3128,7 @@ struct LaunchOwner {
       }
       int per = dev >= 0 && dev < 16 ? resident[dev] : 4;
       if (WV_OWNER_PER_SM > 0 && per > WV_OWNER_PER_SM) per = WV_OWNER_PER_SM;
+      if (grid > 0 && (int)grid < per) per = (int)grid;  // caller's CTAs-per-SM cap (split owner part B)
       const unsigned g = (unsigned)(sms * per);
       sgns_owner_flat_kernel<T, EPC, MAXC><<<g, 256, 0, st>>>(a);
       WV_LAUNCH_CHECK();
@@ -3459,9 +3483,10 @@ static PairArgs pair_args(const BatchCtx& c, int h) {
   pa.Vl = c.V;
   pa.V = c.Vtok;
   pa.desc = c.bw.desc;
-  pa.U = c.bw.U;
-  pa.G = c.bw.G;
-  pa.coef = c.bw.coef;
+  pa.U = c.bw.U[h];
+  pa.G = c.bw.G[h];
+  pa.coef = c.bw.coef[h];
+  pa.flag = c.bw.half[h].flag;
   pa.cnt = c.bw.half[h].cnt;
   pa.uniq = c.bw.half[h].uniq;
   pa.gctr = c.bw.half[h].gctr;
@@ -3495,6 +3520,42 @@ static int enqueue_decode(const BatchCtx& c, int h, cudaStream_t st) {
   return 0;
 }
 
+// Split owner (pipelined batches): batch i's light rows are regrouped into the
+// rows batch i + 1 also touches (A: front of segs2) and the rest (B: back).
+// A is applied before batch i + 1's gather; B runs concurrently with that
+// gather, which never reads a B row (and batch i + 2's gather waits for B).
+__global__ void split_light(const Segment* __restrict__ segs, uint32_t* gctr, const uint8_t* __restrict__ next_flag,
+                            Segment* __restrict__ segs2) {
+  const uint32_t n = *(volatile const uint32_t*)(gctr + GC_LIGHT);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const bool ok = i < n;
+    Segment sg;
+    bool in_a = false;
+    if (ok) {
+      sg = segs[i];
+      in_a = next_flag[sg.key] != 0;
+    }
+    const uint32_t ma = __ballot_sync(0xffffffffu, ok && in_a);
+    const uint32_t mb = __ballot_sync(0xffffffffu, ok && !in_a);
+    uint32_t pa = 0, pb = 0;
+    if (lane == 0) {
+      if (ma) pa = atomicAdd(gctr + GC_NA, (uint32_t)__popc(ma));
+      if (mb) pb = atomicAdd(gctr + GC_NB, (uint32_t)__popc(mb));
+    }
+    pa = __shfl_sync(0xffffffffu, pa, 0);
+    pb = __shfl_sync(0xffffffffu, pb, 0);
+    const uint32_t below = (1u << lane) - 1u;
+    if (ok) {
+      if (in_a)
+        segs2[pa + __popc(ma & below)] = sg;
+      else
+        segs2[n - 1u - (pb + __popc(mb & below))] = sg;
+    }
+  }
+}
+
 static OwnerArgs owner_args(const BatchCtx& c, int h) {
   const WvSgnsModel* model = c.model;
   const BatchHalf& x = c.bw.half[h];
@@ -3520,9 +3581,12 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
   oa.segs = x.segs;
   oa.heavy = x.heavy;
   oa.seg_count = x.gctr + GC_LIGHT;
-  oa.U = c.bw.U;
-  oa.G = c.bw.G;
-  oa.coef = c.bw.coef;
+  oa.U = c.bw.U[h];
+  oa.G = c.bw.G[h];
+  oa.coef = c.bw.coef[h];
+  oa.flag = x.flag;
+  oa.seg_base = nullptr;
+  oa.bookkeep = 1;
   oa.in = model->input;
   oa.out = model->output;
   oa.m_in = model->m_in;
@@ -3595,12 +3659,25 @@ struct LaunchPieces {
 
 // owner phase: heavy rows on ss->h concurrently with the light rows on `st`,
 // then (split mode) the Adam pass and (dense mode) the dense Adam sweep
+// part: 0 = the whole batch; 1 = split part A (heavy pieces + light rows the next
+// batch touches, from segs2); 2 = split part B (the other light rows, on ss->b)
 static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t st, int t_light = -1,
-                          int t_heavy = -1) {
+                          int t_heavy = -1, int part = 0) {
   const WvSgnsModel* model = c.model;
   const int64_t V = c.V, items = c.items;
   const int d = c.d;
-  const OwnerArgs oa = owner_args(c, h);
+  OwnerArgs oa = owner_args(c, h);
+  if (part == 2) {
+    oa.segs = c.bw.half[h].segs2;
+    oa.seg_count = c.bw.half[h].gctr + GC_NB;
+    oa.seg_base = c.bw.half[h].gctr + GC_NA;
+    oa.bookkeep = 0;
+    return dispatch_rows<LaunchOwner>(model->precision, d, oa, (unsigned)WV_SPLIT_B_PER_SM, st);
+  }
+  if (part == 1) {
+    oa.segs = c.bw.half[h].segs2;
+    oa.seg_count = c.bw.half[h].gctr + GC_NA;
+  }
   if (flat_owner(c)) {
     if (WV_OWNER_FUSED_HEAVY) return dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
     // heavy pieces on the side stream (small footprint), concurrent with the light rows
@@ -3732,30 +3809,62 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
   WV_CUDA_RC(bind_if_eager(batch, c, st));
   SideStream* ss = nullptr;
   WV_CUDA(side_stream(&ss));
+  const bool split = WV_SPLIT_OWNER && flat_owner(c) && !WV_OWNER_FUSED_HEAVY && getenv("WV_NO_SPLIT") == nullptr;
   WV_CUDA(cudaEventRecord(ss->fork, st));
   WV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   // optional timeline (profiling): per batch i, slots timer_base + 7i + {0 side start,
-  // 1 side end, 2 gather start, 3 gather end, 4 update end, 5 light-row owner end,
-  // 6 heavy pieces end}
+  // 1 side end, 2 gather start, 3 gather end, 4 update end (part A when split), 5 light-row
+  // owner end, 6 heavy pieces end}
+  auto side_batch = [&](int64_t j) -> int {  // decode + grouping of batch j on the side stream
+    const int hj = (int)(j & 1);
+    const int tj = 7 * (int)j;
+    if (j >= 2) {  // half hj was batch j-2's: its update (main part and B part) must be done
+      WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[hj], 0));
+      WV_CUDA(cudaStreamWaitEvent(ss->s, ss->bdone[hj], 0));
+    }
+    WV_STAMP(tj + 0, ss->s);
+    WV_CUDA_RC(enqueue_decode(c, hj, ss->s));
+    WV_CUDA(cudaEventRecord(ss->dec[hj], ss->s));
+    WV_CUDA_RC(enqueue_group(c, hj, ss->s));
+    WV_STAMP(tj + 1, ss->s);
+    WV_CUDA(cudaEventRecord(ss->grp[hj], ss->s));
+    return 0;
+  };
+  WV_CUDA_RC(side_batch(0));
   for (int64_t i = 0; i < count; ++i) {
     const int h = (int)(i & 1);
     const int t0 = 7 * (int)i;
-    if (i >= 2) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[h], 0));
-    WV_STAMP(t0 + 0, ss->s);
-    WV_CUDA_RC(enqueue_decode(c, h, ss->s));
-    WV_CUDA(cudaEventRecord(ss->dec[h], ss->s));
-    WV_CUDA_RC(enqueue_group(c, h, ss->s));
-    WV_STAMP(t0 + 1, ss->s);
-    WV_CUDA(cudaEventRecord(ss->grp[h], ss->s));
     WV_CUDA(cudaStreamWaitEvent(st, ss->dec[h], 0));
+    // batch i-2's B rows may be rows of this batch (and half h's U/G is theirs)
+    if (i >= 2) WV_CUDA(cudaStreamWaitEvent(st, ss->bdone[h], 0));
     WV_STAMP(t0 + 2, st);
     WV_CUDA_RC(enqueue_gather(c, h, st));
     WV_STAMP(t0 + 3, st);
+    // the next batch's decode (its row flags) and grouping overlap this batch
+    if (i + 1 < count) WV_CUDA_RC(side_batch(i + 1));
     WV_CUDA(cudaStreamWaitEvent(st, ss->grp[h], 0));
-    WV_CUDA_RC(enqueue_update(c, h, ss, st, c.timer ? t0 + 5 : -1, c.timer ? t0 + 6 : -1));
+    if (split && i + 1 < count) {
+      // regroup this batch's light rows by membership in batch i+1 (its decode is done)
+      WV_CUDA(cudaStreamWaitEvent(st, ss->dec[h ^ 1], 0));
+      split_light<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(c.bw.half[h].segs, c.bw.half[h].gctr,
+                                                                   c.bw.half[h ^ 1].flag, c.bw.half[h].segs2);
+      WV_LAUNCH_CHECK();
+      // part B on its own stream: never read by batch i+1; batch i+2 waits for it
+      WV_CUDA(cudaEventRecord(ss->fork_b, st));
+      WV_CUDA(cudaStreamWaitEvent(ss->b, ss->fork_b, 0));
+      WV_CUDA_RC(enqueue_update(c, h, ss, ss->b, -1, -1, 2));
+      WV_CUDA(cudaEventRecord(ss->bdone[h], ss->b));
+      WV_CUDA_RC(enqueue_update(c, h, ss, st, c.timer ? t0 + 5 : -1, c.timer ? t0 + 6 : -1, 1));
+    } else {
+      WV_CUDA_RC(enqueue_update(c, h, ss, st, c.timer ? t0 + 5 : -1, c.timer ? t0 + 6 : -1, 0));
+      WV_CUDA(cudaEventRecord(ss->bdone[h], st));
+    }
     WV_STAMP(t0 + 4, st);
     WV_CUDA(cudaEventRecord(ss->own[h], st));
   }
+  // join: the last B parts and the side stream
+  if (count >= 2) WV_CUDA(cudaStreamWaitEvent(st, ss->bdone[(count - 2) & 1], 0));
+  WV_CUDA(cudaStreamWaitEvent(st, ss->bdone[(count - 1) & 1], 0));
   WV_CUDA(cudaEventRecord(ss->join, ss->s));
   WV_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
   return 0;
@@ -3930,9 +4039,9 @@ int wv_shard_update(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
   using namespace wv;
   BatchCtx c;
   WV_CUDA_RC(shard_ctx(model, batch, ws, ws_bytes, vocab_global, nshard, shard, c));
-  c.bw.U = const_cast<void*>(U);
-  c.bw.G = const_cast<void*>(G);
-  c.bw.coef = const_cast<void*>(coef);
+  c.bw.U[0] = const_cast<void*>(U);
+  c.bw.G[0] = const_cast<void*>(G);
+  c.bw.coef[0] = const_cast<void*>(coef);
   SideStream* ss = nullptr;
   WV_CUDA(side_stream(&ss));
   return enqueue_update(c, 0, ss, (cudaStream_t)stream);
