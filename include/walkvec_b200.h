@@ -333,6 +333,15 @@ int wv_format_plan(const void* vec, int precision, int64_t rows, int d, const in
 int wv_format_emit(const char* lex, const int64_t* lex_off, int64_t rows, int d, char sep, char* out, void* ws,
                    int64_t ws_bytes, void* stream);
 int wv_wvc1_pack(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, uint32_t* body, void* stream);
+/* WVC1 reader (load_corpus_binary, walks.py:368-389): the body words after the
+ * 12-byte header -> offsets [count + 1] and tokens [n_words - count].  Records
+ * are located by speculative chunk parsing (any record length; records of 128
+ * words or more take a sequential path).  *status (device int): 0 ok, 2 corrupt
+ * (a record runs past the body, or words remain after `count` records), 3 the
+ * body ends before `count` records. */
+int64_t wv_wvc1_read_workspace_bytes(int64_t n_words);
+int wv_wvc1_read(const uint32_t* body, int64_t n_words, int64_t count, int64_t* offsets, int32_t* tokens, int* status,
+                 void* ws, int64_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------ synthetic --
  * Measurement inputs (BASELINE.json configs).  gen_barabasi restates

@@ -151,6 +151,8 @@ SIGNATURES = {
     "wv_candidates": (I32, [P, I64, I64, P, P, P, P, I64, P]),
     "wv_sgns_epoch_begin": (I32, [P, I64, I64, P]),
     "wv_sgns_decode": (I32, [P, I64, I64, I64, P, P, P]),
+    "wv_wvc1_read_workspace_bytes": (I64, [I64]),
+    "wv_wvc1_read": (I32, [P, I64, I64, P, P, P, P, I64, P]),
     "wv_shard_count_requests": (I32, [P, I64, I64, I64, I32, P, P, P]),
     "wv_sgns_batch_workspace_bytes": (I64, [I64, I32, I32, I64, I32, I32]),
     "wv_sgns_workspace_init": (I32, [P, I64, I64, I32, I32, I64, I32, I32, P]),

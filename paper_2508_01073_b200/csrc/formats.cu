@@ -224,6 +224,121 @@ __global__ void wvc1_pack(const int32_t* __restrict__ tokens, const int64_t* __r
   }
 }
 
+
+// ------------------------------------------------------------ WVC1 reader ---
+// load_corpus_binary (walks.py:368-389): the body is a chain of records
+// [len, tok_1 .. tok_len]; record r's header position depends on every earlier
+// length.  Speculative chunk parsing: the body is cut into chunks of kRdChunk
+// words; for each chunk and each candidate entry offset j < kRdCand (the first
+// header at or after the chunk start lies within kRdCand words of it whenever
+// records are shorter than kRdCand), one thread parses the chunk and records
+// where the chain leaves it and how many records started inside.  One thread
+// then follows the true entries chunk to chunk (one table lookup per chunk);
+// every chunk is finally re-parsed from its true entry to emit offsets and
+// tokens.  A record of kRdCand words or more sends the whole file to a
+// sequential single-thread parse (correct for any file, slow).
+constexpr int kRdChunk = 8192;
+constexpr int kRdCand = 128;
+
+static inline int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
+
+__global__ void wvc1_spec(const uint32_t* __restrict__ body, int64_t n, int64_t n_chunks, int32_t* __restrict__ exit_off,
+                          int32_t* __restrict__ nrec) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_chunks * kRdCand) return;
+  const int64_t c = t / kRdCand;
+  const int j = (int)(t - c * kRdCand);
+  const int64_t s0 = c * kRdChunk;
+  const int64_t s1 = s0 + kRdChunk < n ? s0 + kRdChunk : n;  // the last chunk ends at the body's end
+  int64_t p = s0 + j;
+  int32_t cnt = 0, ex;
+  bool long_rec = false;
+  while (p < s1) {
+    const uint32_t L = body[p];
+    if ((int64_t)L + 1 >= kRdCand) {
+      long_rec = true;
+      break;
+    }
+    p += 1 + (int64_t)L;
+    ++cnt;
+  }
+  // exit: -2 a record of kRdCand words or more; -1 the chain runs past the body;
+  // else the entry offset into the next chunk (0 at the body's end = a clean end)
+  if (long_rec) ex = -2;
+  else if (p > n) ex = -1;
+  else ex = (int32_t)(p - s1);
+  exit_off[t] = ex;
+  nrec[t] = cnt;
+}
+
+// follow the chain: chunk c's true entry offset and first record index; status 0 ok,
+// 1 a long record (sequential fallback), 2 corrupt (overrun or trailing words),
+// 3 the body ends before `count` records
+__global__ void wvc1_resolve(const int32_t* __restrict__ exit_off, const int32_t* __restrict__ nrec, int64_t n_chunks,
+                             int64_t count, int32_t* __restrict__ entry, int64_t* __restrict__ rec_base, int* status) {
+  int64_t e = 0, r = 0;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    entry[c] = (int32_t)e;
+    rec_base[c] = r;
+    const int32_t ex = exit_off[c * kRdCand + e];
+    if (ex == -2) {
+      *status = 1;
+      return;
+    }
+    if (ex == -1) {
+      *status = 2;
+      return;
+    }
+    r += nrec[c * kRdCand + e];
+    e = ex;
+  }
+  *status = e != 0 ? 2 : (r == count ? 0 : (r < count ? 3 : 2));
+}
+
+__global__ void wvc1_emit(const uint32_t* __restrict__ body, int64_t n, int64_t n_chunks,
+                          const int32_t* __restrict__ entry, const int64_t* __restrict__ rec_base,
+                          int64_t* __restrict__ offsets, int32_t* __restrict__ tokens) {
+  // warp per chunk: lane 0 walks the headers, the warp copies each record's tokens
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < n_chunks; c += nw) {
+    const int64_t s1 = (c + 1) * kRdChunk;
+    int64_t p = c * kRdChunk + entry[c];
+    int64_t r = rec_base[c];
+    while (p < s1 && p < n) {
+      const int64_t L = body[p];
+      if (lane == 0) offsets[r + 1] = p + 1 + L - (r + 1);  // tokens before record r + 1
+      for (int64_t q = lane; q < L; q += 32) tokens[p + 1 + q - (r + 1)] = (int32_t)body[p + 1 + q];
+      p += 1 + L;
+      ++r;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) offsets[0] = 0;
+}
+
+// any-length fallback: one thread, the reference's own loop
+__global__ void wvc1_sequential(const uint32_t* __restrict__ body, int64_t n, int64_t count,
+                                int64_t* __restrict__ offsets, int32_t* __restrict__ tokens, int* status) {
+  int64_t p = 0, pos = 0;
+  offsets[0] = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    if (p >= n) {
+      *status = 3;
+      return;
+    }
+    const int64_t L = body[p];
+    if (p + 1 + L > n) {
+      *status = 2;
+      return;
+    }
+    for (int64_t q = 0; q < L; ++q) tokens[pos + q] = (int32_t)body[p + 1 + q];
+    p += 1 + L;
+    pos += L;
+    offsets[i + 1] = pos;
+  }
+  *status = p == n ? 0 : 2;
+}
 }  // namespace wv
 
 extern "C" {
@@ -292,4 +407,55 @@ int wv_wvc1_pack(const int32_t* tokens, const int64_t* offsets, int64_t n_walks,
   return 0;
 }
 
+
+int64_t wv_wvc1_read_workspace_bytes(int64_t n_words) {
+  const int64_t chunks = (n_words + wv::kRdChunk - 1) / wv::kRdChunk;
+  return 2 * wv::al256(chunks * wv::kRdCand * 4) + wv::al256(chunks * 4) + wv::al256(chunks * 8) + 256 + 1024;
+}
+
+int wv_wvc1_read(const uint32_t* body, int64_t n_words, int64_t count, int64_t* offsets, int32_t* tokens, int* status,
+                 void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(n_words >= 0 && count >= 0, "bad sizes");
+  WV_CHECK_ARG(ws_bytes >= wv_wvc1_read_workspace_bytes(n_words), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t chunks = (n_words + kRdChunk - 1) / kRdChunk;
+  char* w = (char*)ws;
+  int32_t* exit_off = (int32_t*)w;
+  w += al256(chunks * kRdCand * 4);
+  int32_t* nrec = (int32_t*)w;
+  w += al256(chunks * kRdCand * 4);
+  int32_t* entry = (int32_t*)w;
+  w += al256(chunks * 4);
+  int64_t* rec_base = (int64_t*)w;
+  WV_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+  if (n_words == 0) {
+    WV_CUDA(cudaMemsetAsync(offsets, 0, 8, st));
+    if (count != 0) {
+      static const int three = 3;  // the body ends before `count` records
+      WV_CUDA(cudaMemcpyAsync(status, &three, sizeof(int), cudaMemcpyHostToDevice, st));
+      WV_CUDA(cudaStreamSynchronize(st));
+    }
+    return 0;
+  }
+  const int64_t nt = chunks * kRdCand;
+  wvc1_spec<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(body, n_words, chunks, exit_off, nrec);
+  WV_LAUNCH_CHECK();
+  wvc1_resolve<<<1, 1, 0, st>>>(exit_off, nrec, chunks, count, entry, rec_base, status);
+  WV_LAUNCH_CHECK();
+  int h_status = 0;
+  WV_CUDA(cudaMemcpyAsync(&h_status, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WV_CUDA(cudaStreamSynchronize(st));
+  if (h_status == 1) {
+    WV_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    wvc1_sequential<<<1, 1, 0, st>>>(body, n_words, count, offsets, tokens, status);
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+  if (h_status != 0) return 0;  // corrupt: the caller raises (status stays 2)
+  const unsigned g = (unsigned)((chunks * 32 + 255) / 256 < 148 * 16 ? (chunks * 32 + 255) / 256 : 148 * 16);
+  wvc1_emit<<<g, 256, 0, st>>>(body, n_words, chunks, entry, rec_base, offsets, tokens);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
 }  // extern "C"

@@ -1773,7 +1773,7 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
 #define WV_FLAT_U 1
 #endif
 #ifndef WV_FLAT_MINB
-#define WV_FLAT_MINB 5
+#define WV_FLAT_MINB 4  // 64 registers, no spill stack (48 spilled 40 B): fp64 owner 297 -> 290 us
 #endif
 #ifndef WV_OWNER_FUSED_HEAVY
 #define WV_OWNER_FUSED_HEAVY 0
@@ -2108,10 +2108,10 @@ template <typename T, int EPC, int MAXC>
 #define WV_SPLIT_B_PER_SM 2  // split owner: B-row CTAs per SM (they share the SMs with the next gather)
 #endif
 #ifndef WV_SPLIT_OWNER
-#define WV_SPLIT_OWNER 1  // pipelined batches: apply the next batch's rows first, the rest beside its gather
+#define WV_SPLIT_OWNER 0  // measured: the B rows starve the concurrent gather (97 -> 307 us), 60.4 -> 44.7 M pairs/s fp64
 #endif
 #ifndef WV_OWNER_PER_SM
-#define WV_OWNER_PER_SM 4  // light-row owner CTAs per SM (room for the concurrent heavy pieces); 0: all resident
+#define WV_OWNER_PER_SM 3  // light-row owner CTAs per SM (room for the concurrent heavy pieces); 0: all resident
 #endif
 __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kernel(OwnerArgs A) {
   constexpr int W = kHeavyThreads / 32;

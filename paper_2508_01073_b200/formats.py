@@ -100,3 +100,43 @@ def save_corpus_binary(corpus, path):
         fh.write(_CORPUS_MAGIC)
         fh.write(struct.pack("<BBHI", strategies[corpus.strategy], projections[corpus.projection], 0, n))
         fh.write(body[: n + total].cpu().numpy().astype("<u4").tobytes())
+
+
+def load_corpus_binary(path):
+    """Read a WVC1 walk corpus (walks.py:368-389) into a device WalkCorpus.
+
+    The file is read once; record boundaries (a chain of u32 length headers)
+    are found on the device by speculative chunk parsing (csrc/formats.cu).
+    Errors follow the reference: ValueError for a bad magic or a corrupt body,
+    IndexError when the body ends before the header's walk count.
+    """
+    from .walks import BFS, ENTITY, FULL, PROPERTY, RANDOM, WalkCorpus
+
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    raw = open(path, "rb").read()
+    if raw[:4] != _CORPUS_MAGIC:
+        raise ValueError("not a walk corpus file")
+    strategy_b, projection_b, _, count = struct.unpack("<BBHI", raw[4:12])
+    strategies = {0: RANDOM, 1: BFS}
+    projections = {0: FULL, 1: ENTITY, 2: PROPERTY}
+    if (len(raw) - 12) % 4:
+        raise ValueError("buffer size must be a multiple of element size")
+    n = (len(raw) - 12) // 4
+    body = torch.frombuffer(bytearray(raw[12:]), dtype=torch.int32).to(dev) if n else \
+        torch.zeros(1, dtype=torch.int32, device=dev)
+    n_tok = max(n - count, 0)
+    offsets = torch.empty(count + 1, dtype=torch.int64, device=dev)
+    tokens = torch.empty(max(n_tok, 1), dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(_lib.query("wv_wvc1_read_workspace_bytes", n), dtype=torch.uint8, device=dev)
+    _lib.call("wv_wvc1_read", _lib.ptr(body), n, count, _lib.ptr(offsets), _lib.ptr(tokens), _lib.ptr(status),
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    st = int(status.item())
+    if st == 3:
+        raise IndexError(f"index {n} is out of bounds for axis 0 with size {n}")
+    if st != 0 or (count == 0 and n != 0):
+        raise ValueError("corrupt walk corpus file")
+    if n_tok and int(tokens[:n_tok].min()) < 0:
+        raise ValueError("token out of int32 range")
+    return WalkCorpus.from_device(tokens, offsets, count, n_tok, strategies[strategy_b], projections[projection_b])

@@ -7,7 +7,7 @@ walks_mod.random_walks / bfs_walks (pipeline.py:20, 167, 178), and
 (cli.py:21, 169) and re-exported from the package.  install() swaps exactly
 those attributes, plus ``load_data`` (pipeline.py:117, cli.py:103; GPU ingest)
 and the artifact writers save_embeddings_text / _tsv and save_corpus_binary
-(device-formatted, byte-identical files);
+(device-formatted, byte-identical files) and load_corpus_binary (device parse);
 uninstall() restores them.
 """
 
@@ -94,6 +94,9 @@ def install(package: str = "walkvec", *, precision: str = "fp64", pairs: str = "
         (pipe_mod, "save_embeddings_text", dev_formats.save_embeddings_text),
         (pipe_mod, "save_embeddings_tsv", dev_formats.save_embeddings_tsv),
         (walks_mod, "save_corpus_binary", dev_formats.save_corpus_binary),
+        (walks_mod, "load_corpus_binary", dev_formats.load_corpus_binary),
+        (pkg, "save_corpus_binary", dev_formats.save_corpus_binary),
+        (pkg, "load_corpus_binary", dev_formats.load_corpus_binary),
         (pkg, "load_data", _wrap_load_data(dev_load_data, package)),
     ]
     try:

@@ -63,3 +63,64 @@ def test_wvc1_writer_byte_exact(tmp_path):
     c = wv.WalkCorpus(np.array(G["wvc1_tokens"]), np.array(G["wvc1_offsets"]), wv.BFS, wv.ENTITY)
     formats.save_corpus_binary(c, tmp_path / "c.wvc")
     assert (tmp_path / "c.wvc").read_bytes() == base64.b64decode(G["wvc1"])
+
+
+def _wvc1_bytes(seqs, strategy=0, projection=0, count=None):
+    import struct
+
+    body = []
+    for s in seqs:
+        body.append(len(s))
+        body.extend(s)
+    hdr = b"WVC1" + struct.pack("<BBHI", strategy, projection, 0, len(seqs) if count is None else count)
+    return hdr + np.array(body, dtype="<u4").tobytes()
+
+
+def test_wvc1_reader_reference_fixture(tmp_path):
+    """The reference's own WVC1 file (tests/golden/formats.json) reads back to its corpus."""
+    import paper_2508_01073_b200 as wv
+    from paper_2508_01073_b200 import formats
+
+    (tmp_path / "c.wvc").write_bytes(base64.b64decode(G["wvc1"]))
+    c = formats.load_corpus_binary(tmp_path / "c.wvc")
+    assert np.array_equal(c.tokens, np.array(G["wvc1_tokens"])) and np.array_equal(c.offsets, G["wvc1_offsets"])
+    assert c.strategy == wv.BFS and c.projection == wv.ENTITY
+
+
+@pytest.mark.parametrize("n,maxlen,seed", [(0, 1, 0), (1, 5, 1), (1000, 9, 2), (200_000, 33, 3), (30_000, 300, 4),
+                                           (50_000, 140, 5)])
+def test_wvc1_reader_round_trip(tmp_path, n, maxlen, seed):
+    """Random corpora across chunk boundaries (8192-word chunks, 128-word speculation window),
+    empty walks, and records longer than the window (the sequential path) read back exactly,
+    equal to the reference's reader restated (walks.py:368-389)."""
+    from paper_2508_01073_b200 import formats
+
+    rng = np.random.default_rng(seed)
+    seqs = [rng.integers(0, 2**31 - 1, rng.integers(0, maxlen + 1)).tolist() for _ in range(n)]
+    (tmp_path / "r.wvc").write_bytes(_wvc1_bytes(seqs, 1, 2))
+    c = formats.load_corpus_binary(tmp_path / "r.wvc")
+    lens = np.array([len(s) for s in seqs], dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    tok = np.array([t for s in seqs for t in s], dtype=np.int64)
+    assert len(c) == n and np.array_equal(c.offsets, off) and np.array_equal(c.tokens, tok)
+
+
+def test_wvc1_reader_errors(tmp_path):
+    """Reference error behaviour: bad magic -> ValueError; words left after `count` records or a
+    record running past the body -> ValueError; the body ending before `count` records -> IndexError."""
+    from paper_2508_01073_b200 import formats
+
+    p = tmp_path / "e.wvc"
+    p.write_bytes(b"WVCX" + _wvc1_bytes([[1]])[4:])
+    with pytest.raises(ValueError, match="not a walk corpus file"):
+        formats.load_corpus_binary(p)
+    p.write_bytes(_wvc1_bytes([[1, 2], [3]], count=1))  # trailing record
+    with pytest.raises(ValueError, match="corrupt"):
+        formats.load_corpus_binary(p)
+    good = _wvc1_bytes([[1, 2], [3]])
+    p.write_bytes(good[:-4])  # the last record runs past the body
+    with pytest.raises(ValueError):
+        formats.load_corpus_binary(p)
+    p.write_bytes(_wvc1_bytes([[1, 2], [3]], count=3))  # fewer records than the header says
+    with pytest.raises(IndexError):
+        formats.load_corpus_binary(p)
