@@ -114,12 +114,43 @@ struct Walker {
 // hop loop interleaves the thread's walkers so their dependent CSR reads
 // (offsets -> packed edge) overlap.  Rows are staged in shared memory and
 // written with 16-byte stores.
+// Per-shard generator seeds (SeedSequence([seed, 0, s]) -> PCG64 state + inc, or
+// the Philox key), computed once per shard of the launch instead of once per CTA:
+// a shard spans 16 CTAs of 512 walkers, and the hashing is a serial chain the
+// CTA's other warps wait on.
+#ifndef WV_WALK_SEED_TABLE
+#define WV_WALK_SEED_TABLE 1
+#endif
+template <int RNG>
+__global__ void seed_shards(WalkParams P, int64_t s_first, int64_t n, uint64_t* __restrict__ tab) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint32_t pool[4];
+  ss_pool(P.prefix, P.n_prefix, (uint64_t)(s_first + t), pool);
+  uint64_t* o = tab + 4 * t;
+  if (RNG == WV_RNG_PCG64) {
+    const Pcg64 g = pcg_seed(pool);
+    o[0] = g.state.lo;
+    o[1] = g.state.hi;
+    o[2] = g.inc.lo;
+    o[3] = g.inc.hi;
+  } else {
+    uint64_t key[2];
+    ss_generate_u64(pool, 2, key);
+    o[0] = key[0];
+    o[1] = key[1];
+    o[2] = o[3] = 0;
+  }
+}
+
 #ifndef WV_WALK_MINB
 #define WV_WALK_MINB 4
 #endif
 template <int RNG, int WPT>
 __global__ void __launch_bounds__(kWalkThreads, RNG == WV_RNG_PCG64 ? WV_WALK_MINB : 1) random_walk_kernel(WalkParams P,
-                                                                              const PcgJump* __restrict__ jrows) {
+                                                                              const PcgJump* __restrict__ jrows,
+                                                                              const uint64_t* __restrict__ seeds,
+                                                                              int64_t s_first, int64_t n_seeds) {
   extern __shared__ int32_t stage[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int width = P.width;
@@ -128,7 +159,12 @@ __global__ void __launch_bounds__(kWalkThreads, RNG == WV_RNG_PCG64 ? WV_WALK_MI
   // lanes 0/1 of warp 0 seed them once for the whole CTA
   __shared__ uint64_t sh_seed[2][4];  // PCG64: state.lo, state.hi, inc.lo, inc.hi; Philox: key
   const int64_t s0 = (P.work_begin + blk0) / kShard;
-  if (warp == 0 && lane < 2) {
+  if (seeds != nullptr) {
+    if (threadIdx.x < 8) {  // two shards x four words from the launch's seed table
+      const int64_t t = s0 + (threadIdx.x >> 2) - s_first;
+      if (t < n_seeds) sh_seed[threadIdx.x >> 2][threadIdx.x & 3] = seeds[4 * t + (threadIdx.x & 3)];
+    }
+  } else if (warp == 0 && lane < 2) {
     uint32_t pool[4];
     ss_pool(P.prefix, P.n_prefix, (uint64_t)(s0 + lane), pool);
     if (RNG == WV_RNG_PCG64) {
@@ -430,10 +466,22 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, in
   const int64_t per_block = (int64_t)kWalkThreads * wpt;
   const int64_t blocks = (work_count + per_block - 1) / per_block;
   WV_CHECK_ARG(blocks < (1ll << 31), "too many walkers for one launch");
+  uint64_t* seeds = nullptr;
+  const int64_t s_first = work_begin / kShard;
+  const int64_t n_seeds = work_count > 0 ? (work_begin + work_count - 1) / kShard - s_first + 1 : 0;
+  if (WV_WALK_SEED_TABLE && n_seeds > 0) {
+    // stream-ordered scratch (freed after the walk kernel on the same stream)
+    WV_CUDA(cudaMallocAsync((void**)&seeds, (size_t)n_seeds * 32, st));
+    if (rng_kind == WV_RNG_PCG64)
+      seed_shards<WV_RNG_PCG64><<<(unsigned)((n_seeds + 127) / 128), 128, 0, st>>>(P, s_first, n_seeds, seeds);
+    else
+      seed_shards<WV_RNG_PHILOX><<<(unsigned)((n_seeds + 127) / 128), 128, 0, st>>>(P, s_first, n_seeds, seeds);
+    WV_LAUNCH_CHECK();
+  }
   auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024)
       WV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)blocks, kWalkThreads, smem, st>>>(P, jrows);
+    kern<<<(unsigned)blocks, kWalkThreads, smem, st>>>(P, jrows, seeds, s_first, n_seeds);
     return 0;
   };
   int rc;
@@ -443,6 +491,7 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, in
     rc = two ? launch(random_walk_kernel<WV_RNG_PHILOX, 2>) : launch(random_walk_kernel<WV_RNG_PHILOX, 1>);
   if (rc) return rc;
   WV_LAUNCH_CHECK();
+  if (seeds) WV_CUDA(cudaFreeAsync(seeds, st));
   return 0;
 }
 
