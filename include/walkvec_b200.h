@@ -315,7 +315,7 @@ int wv_ingest_lines(const uint8_t* text, int64_t n_bytes, int64_t* line_end, int
                     int64_t ws_bytes, void* stream);
 int64_t wv_ingest_workspace_bytes(int64_t n_lines);
 int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_end, int64_t n_lines, int mode,
-                    int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
+                    uint64_t hash_seed, int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
                     int64_t* bad, int64_t* n_out, int64_t* edges, uint32_t* roles, int64_t* tok_span, void* ws,
                     int64_t ws_bytes, void* stream);
 

@@ -105,16 +105,16 @@ struct KeyIter {
   }
 };
 
-__device__ uint64_t key_hash(const uint8_t* text, int64_t s, int64_t t, bool esc) {
+__device__ uint64_t key_hash(const uint8_t* text, int64_t s, int64_t t, bool esc, uint64_t seed) {
   KeyIter it(text, s, t, esc);
-  uint64_t h = 0xcbf29ce484222325ull;
+  uint64_t h = 0xcbf29ce484222325ull ^ (seed ? splitmix64(seed) : 0ull);
   uint64_t n = 0;
   uint8_t b;
   while (it.next(b)) {
     h = (h ^ b) * 0x100000001b3ull;
     ++n;
   }
-  h = splitmix64(h ^ (n * 0x9E3779B97F4A7C15ull));
+  h = splitmix64(h ^ (n * 0x9E3779B97F4A7C15ull) ^ (seed * 0xD6E8FEB86659FD93ull));
   return h ? h : 1ull;  // 0 marks an empty table slot
 }
 
@@ -394,6 +394,7 @@ struct Table {
   unsigned long long* first;  // first occurrence position
   int64_t* token;
   uint64_t mask;
+  uint64_t seed;  // hash seed: a collision (reported, never merged) is retried with another seed
 };
 
 __device__ __forceinline__ bool occ_active(const Term* occ, int64_t pos, int include_literals) {
@@ -406,7 +407,7 @@ __global__ void ingest_insert(const uint8_t* __restrict__ text, const Term* __re
        pos += (int64_t)gridDim.x * blockDim.x) {
     if (!occ_active(occ, pos, include_literals)) continue;
     const Term tm = occ[pos];
-    const unsigned long long h = key_hash(text, tm.s, tm.t, tm.esc);
+    const unsigned long long h = key_hash(text, tm.s, tm.t, tm.esc, T.seed);
     uint64_t slot = h & T.mask;
     while (true) {
       const unsigned long long prev = atomicCAS(T.key + slot, 0ull, h);
@@ -542,6 +543,7 @@ int64_t wv_ingest_workspace_bytes(int64_t n_lines) {
 }
 
 int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_end, int64_t n_lines, int mode,
+                    uint64_t hash_seed,
                     int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
                     int64_t* bad, int64_t* n_out, int64_t* edges, uint32_t* roles, int64_t* tok_span, void* ws,
                     int64_t ws_bytes, void* stream) {
@@ -568,6 +570,7 @@ int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_en
   uint8_t* kept = (uint8_t*)take(n_lines);
   int64_t* scan_ws = (int64_t*)take(scan_tiles(n_lines + 1) * 8);
   Table T;
+  T.seed = hash_seed;
   T.key = (unsigned long long*)take(cap * 8);
   T.first = (unsigned long long*)take(cap * 8);
   T.token = (int64_t*)take(cap * 8);

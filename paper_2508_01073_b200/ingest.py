@@ -196,6 +196,9 @@ def _read_bytes(source) -> bytes:
     return data.encode("utf-8") if isinstance(data, str) else data
 
 
+_HASH_ATTEMPTS = 4
+
+
 def load_triples_device(source, format: str = "nt", *, strict: bool = False, error_sink: list | None = None,
                         include_literals: bool = False, has_header: bool = False, device=None):
     """Parse + tokenize on the GPU: (Vocabulary, (E,3) int64 edges).
@@ -238,11 +241,17 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
     roles = torch.empty(max(3 * n_lines, 1), dtype=torch.int32, device=dev)
     tok_span = torch.empty(max(9 * n_lines, 3), dtype=torch.int64, device=dev)
     ws = torch.empty(_lib.query("wv_ingest_workspace_bytes", n_lines), dtype=torch.uint8, device=dev)
-    _lib.call("wv_ingest_parse", _lib.ptr(text), n, _lib.ptr(line_end), n_lines, _MODES[format], _DELIM[format],
-              int(has_header), int(include_literals), _lib.ptr(status), _lib.ptr(err), _lib.ptr(err_at),
-              _lib.ptr(bad), _lib.ptr(n_out), _lib.ptr(edges), _lib.ptr(roles), _lib.ptr(tok_span), _lib.ptr(ws),
-              ws.numel(), st)
-    n_stmt, n_edges, n_tok, collision = (int(x) for x in n_out.cpu().tolist())
+    for hash_seed in range(_HASH_ATTEMPTS):
+        # a 64-bit key-hash collision (distinct keys, equal hashes) is detected, never merged:
+        # re-intern with an independently seeded hash
+        n_out.zero_()
+        _lib.call("wv_ingest_parse", _lib.ptr(text), n, _lib.ptr(line_end), n_lines, _MODES[format], hash_seed,
+                  _DELIM[format], int(has_header), int(include_literals), _lib.ptr(status), _lib.ptr(err),
+                  _lib.ptr(err_at), _lib.ptr(bad), _lib.ptr(n_out), _lib.ptr(edges), _lib.ptr(roles),
+                  _lib.ptr(tok_span), _lib.ptr(ws), ws.numel(), st)
+        n_stmt, n_edges, n_tok, collision = (int(x) for x in n_out.cpu().tolist())
+        if not collision:
+            break
     first_bad, first_value = (int(x) for x in bad.cpu().tolist())
     big = (1 << 63) - 1
     if first_bad != big or first_value != big:
@@ -262,7 +271,7 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
         if first_value != big:
             raise ValueError("subject and predicate must be non-empty")
     if collision:
-        raise RuntimeError("64-bit key hash collision in the GPU ingest (distinct keys with equal hashes)")
+        raise RuntimeError(f"64-bit key hash collisions under {_HASH_ATTEMPTS} independent hash seeds")
     if n_stmt == 0:
         raise ValueError("empty graph")
     spans = tok_span[: 3 * n_tok].view(-1, 3).cpu().numpy()
