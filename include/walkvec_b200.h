@@ -84,8 +84,14 @@ int wv_csr_unpack(const uint64_t* packed_edges, int64_t E, int64_t* col_targets,
  * ranges; the union is byte-identical to one call over everything).
  * seed_prefix = u32 words of [rng_seed, 0] (SeedSequence([seed, 0, shard])).
  * corpus: int32 [work_count, 2*depth+1] padded with -1; lengths: int32[work_count]. */
-int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
-                    const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth, int64_t work_begin,
+/* walk adjacency (optional, E < 2^32): per packed edge e, 16 bytes {pred, dst,
+ * row start of dst, out-degree of dst}, so a walk hop is one dependent load
+ * (the chosen edge names the next row) instead of offsets -> edge.  Random
+ * 8-byte CSR reads cost a 64-byte DRAM fetch each (ncu: 113 B/hop at cfg5). */
+int wv_walk_adjacency_build(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
+                            int64_t edge_count, void* walk_adj, void* stream);
+int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, const void* walk_adj,
+                    int64_t vertex_count, const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth, int64_t work_begin,
                     int64_t work_count, const uint32_t* seed_prefix, int n_prefix, int rng_kind, int32_t* corpus,
                     int32_t* lengths, void* stream);
 
@@ -333,6 +339,12 @@ int wv_format_plan(const void* vec, int precision, int64_t rows, int d, const in
 int wv_format_emit(const char* lex, const int64_t* lex_off, int64_t rows, int d, char sep, char* out, void* ws,
                    int64_t ws_bytes, void* stream);
 int wv_wvc1_pack(const int32_t* tokens, const int64_t* offsets, int64_t n_walks, uint32_t* body, void* stream);
+/* Vocabulary TSV (Vocabulary.save_tsv, ingest.py:307-323): one line per token
+ * "<token>\t<lexical, \\ \t \n \r escaped>\t<roles: e if bit 0, p if bit 1>\t<count>\n".
+ * out = NULL: only *total (device int64, the file size) is computed. */
+int64_t wv_vocab_tsv_workspace_bytes(int64_t rows);
+int wv_vocab_tsv(const uint8_t* lex, const int64_t* lex_off, int64_t rows, const uint8_t* roles, const int64_t* counts,
+                 char* out, int64_t* total, void* ws, int64_t ws_bytes, void* stream);
 /* WVC1 reader (load_corpus_binary, walks.py:368-389): the body words after the
  * 12-byte header -> offsets [count + 1] and tokens [n_words - count].  Records
  * are located by speculative chunk parsing (any record length; records of 128

@@ -129,7 +129,8 @@ SIGNATURES = {
     "wv_csr_workspace_bytes": (I64, [I64, I64]),
     "wv_csr_build": (I32, [P, I64, I64, P, P, P, I64, P]),
     "wv_csr_unpack": (I32, [P, I64, P, P, P]),
-    "wv_random_walks": (I32, [P, P, I64, P, I64, I64, I32, I64, I64, P, I32, I32, P, P, P]),
+    "wv_walk_adjacency_build": (I32, [P, P, I64, I64, P, P]),
+    "wv_random_walks": (I32, [P, P, P, I64, P, I64, I64, I32, I64, I64, P, I32, I32, P, P, P]),
     "wv_compact_workspace_bytes": (I64, [I64]),
     "wv_corpus_compact": (I32, [P, P, I64, I32, P, P, I32, P, I64, P]),
     "wv_dedup_workspace_bytes": (I64, [I64]),
@@ -152,6 +153,8 @@ SIGNATURES = {
     "wv_sgns_epoch_begin": (I32, [P, I64, I64, P]),
     "wv_sgns_decode": (I32, [P, I64, I64, I64, P, P, P]),
     "wv_wvc1_read_workspace_bytes": (I64, [I64]),
+    "wv_vocab_tsv_workspace_bytes": (I64, [I64]),
+    "wv_vocab_tsv": (I32, [P, P, I64, P, P, P, P, P, I64, P]),
     "wv_wvc1_read": (I32, [P, I64, I64, P, P, P, P, I64, P]),
     "wv_shard_count_requests": (I32, [P, I64, I64, I64, I32, P, P, P]),
     "wv_sgns_batch_workspace_bytes": (I64, [I64, I32, I32, I64, I32, I32]),

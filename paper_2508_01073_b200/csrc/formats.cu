@@ -339,6 +339,64 @@ __global__ void wvc1_sequential(const uint32_t* __restrict__ body, int64_t n, in
   }
   *status = p == n ? 0 : 2;
 }
+
+// ------------------------------------------------------ vocabulary TSV ----
+// Vocabulary.save_tsv (ingest.py:307-323): per token "<token>\t<lexical with \\,
+// \t, \n, \r escaped>\t<roles e/p>\t<count>\n" (_escape_field, ingest.py:345-346).
+__device__ __forceinline__ int dec_digits(uint64_t v) {
+  int n = 1;
+  while (v >= 10) {
+    v /= 10;
+    ++n;
+  }
+  return n;
+}
+
+__device__ __forceinline__ bool tsv_special(uint8_t c) { return c == '\\' || c == '\t' || c == '\n' || c == '\r'; }
+
+__global__ void vtsv_len(const uint8_t* __restrict__ lex, const int64_t* __restrict__ lex_off, int64_t rows,
+                         const uint8_t* __restrict__ roles, const int64_t* __restrict__ counts, int64_t* __restrict__ len) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = dec_digits((uint64_t)r) + 1;
+    for (int64_t i = lex_off[r]; i < lex_off[r + 1]; ++i) n += tsv_special(lex[i]) ? 2 : 1;
+    n += 1 + ((roles[r] & 1) ? 1 : 0) + ((roles[r] & 2) ? 1 : 0) + 1 + dec_digits((uint64_t)counts[r]) + 1;
+    len[r] = n;
+  }
+}
+
+__device__ __forceinline__ char* put_dec(char* o, uint64_t v) {
+  const int n = dec_digits(v);
+  for (int i = n - 1; i >= 0; --i) {
+    o[i] = (char)('0' + (int)(v % 10));
+    v /= 10;
+  }
+  return o + n;
+}
+
+__global__ void vtsv_emit(const uint8_t* __restrict__ lex, const int64_t* __restrict__ lex_off, int64_t rows,
+                          const uint8_t* __restrict__ roles, const int64_t* __restrict__ counts,
+                          const int64_t* __restrict__ line_off, char* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    char* o = out + line_off[r];
+    o = put_dec(o, (uint64_t)r);
+    *o++ = '\t';
+    for (int64_t i = lex_off[r]; i < lex_off[r + 1]; ++i) {
+      const uint8_t c = lex[i];
+      if (tsv_special(c)) {
+        *o++ = '\\';
+        *o++ = c == '\\' ? '\\' : (c == '\t' ? 't' : (c == '\n' ? 'n' : 'r'));
+      } else {
+        *o++ = (char)c;
+      }
+    }
+    *o++ = '\t';
+    if (roles[r] & 1) *o++ = 'e';
+    if (roles[r] & 2) *o++ = 'p';
+    *o++ = '\t';
+    o = put_dec(o, (uint64_t)counts[r]);
+    *o++ = '\n';
+  }
+}
 }  // namespace wv
 
 extern "C" {
@@ -456,6 +514,35 @@ int wv_wvc1_read(const uint32_t* body, int64_t n_words, int64_t count, int64_t* 
   const unsigned g = (unsigned)((chunks * 32 + 255) / 256 < 148 * 16 ? (chunks * 32 + 255) / 256 : 148 * 16);
   wvc1_emit<<<g, 256, 0, st>>>(body, n_words, chunks, entry, rec_base, offsets, tokens);
   WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int64_t wv_vocab_tsv_workspace_bytes(int64_t rows) {
+  return wv::al256((rows + 1) * 8) + wv::al256(wv::scan_tiles(rows + 1) * 8) + 512;
+}
+
+int wv_vocab_tsv(const uint8_t* lex, const int64_t* lex_off, int64_t rows, const uint8_t* roles, const int64_t* counts,
+                 char* out, int64_t* total, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(rows >= 0, "bad sizes");
+  WV_CHECK_ARG(ws_bytes >= wv_vocab_tsv_workspace_bytes(rows), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int64_t* line = (int64_t*)w;
+  w += al256((rows + 1) * 8);
+  int64_t* sws = (int64_t*)w;
+  if (rows == 0) {
+    WV_CUDA(cudaMemsetAsync(total, 0, 8, st));
+    return 0;
+  }
+  const unsigned g = (unsigned)((rows + 255) / 256 < 148 * 16 ? (rows + 255) / 256 : 148 * 16);
+  vtsv_len<<<g, 256, 0, st>>>(lex, lex_off, rows, roles, counts, line);
+  WV_LAUNCH_CHECK();
+  WV_CUDA(excl_scan<int64_t, int64_t>(line, rows, line, total, sws, st));
+  if (out != nullptr) {
+    vtsv_emit<<<g, 256, 0, st>>>(lex, lex_off, rows, roles, counts, line, out);
+    WV_LAUNCH_CHECK();
+  }
   return 0;
 }
 }  // extern "C"

@@ -48,6 +48,7 @@ __device__ __forceinline__ PcgJump pcg_jump_dev(uint64_t n) {
 struct WalkParams {
   const int64_t* row_offsets;
   const uint64_t* edges;
+  const uint4* adj;  // optional walk adjacency: per edge {pred, dst, first edge of dst, out-degree of dst}
   const int64_t* roots;
   int64_t walk_number;
   double inv_walk_number;
@@ -225,7 +226,57 @@ __global__ void __launch_bounds__(kWalkThreads, RNG == WV_RNG_PCG64 ? WV_WALK_MI
   }
   const int64_t* __restrict__ off = P.row_offsets;
   const uint64_t* __restrict__ edges = P.edges;
-  for (int h = 0; h < P.depth; ++h) {
+  if (P.adj != nullptr) {
+    // one dependent 16-byte load per hop: the chosen edge carries the next vertex's
+    // row start and degree (the CSR offsets are read once, for the root)
+    const uint4* __restrict__ adj = P.adj;
+    uint32_t start[WPT], deg[WPT];
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      start[q] = deg[q] = 0;
+      if (W[q].alive) {
+        const int64_t lo = __ldg(off + W[q].cur), hi = __ldg(off + W[q].cur + 1);
+        start[q] = (uint32_t)lo;
+        deg[q] = (uint32_t)(hi - lo);
+      }
+    }
+    for (int h = 0; h < P.depth; ++h) {
+      uint4 e[WPT];
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        if (W[q].alive && deg[q] == 0) W[q].alive = false;
+        uint64_t u = 0;
+        if (RNG == WV_RNG_PCG64) {
+          u = pcg_output(W[q].x);
+          W[q].x = add128(mul128(W[q].last ? P.stride_last.A : P.stride_full.A, W[q].x), W[q].cstep);
+        } else if (W[q].alive) {
+          const uint64_t n_s = W[q].last ? (uint64_t)P.n_last : (uint64_t)kShard;
+          u = philox_numpy_u64(k0[q], k1[q], (uint64_t)h * n_s + W[q].i);
+        }
+        const int64_t dg = (int64_t)deg[q];
+        int64_t pick = __double2ll_rz(__dmul_rn(u64_to_double(u), (double)dg));
+        if (pick > dg - 1) pick = dg - 1;
+        e[q] = W[q].alive ? __ldg(adj + (int64_t)start[q] + pick) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        if (W[q].alive) {
+          int32_t* my = stage + ((q * kWalkThreads) + warp * 32 + lane) * width;
+          my[2 * h + 1] = (int32_t)e[q].x;
+          my[2 * h + 2] = (int32_t)e[q].y;
+          W[q].cur = (int64_t)e[q].y;
+          start[q] = e[q].z;
+          deg[q] = e[q].w;
+          W[q].len += 2;
+        }
+      }
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) any |= W[q].alive;
+      if (!any) break;
+    }
+  }
+  for (int h = 0; h < (P.adj != nullptr ? 0 : P.depth); ++h) {
     int64_t lo[WPT], hi[WPT];
 #pragma unroll
     for (int q = 0; q < WPT; ++q) {
@@ -291,6 +342,18 @@ __global__ void __launch_bounds__(kWalkThreads, RNG == WV_RNG_PCG64 ? WV_WALK_MI
     } else {
       for (int j = lane; j < total; j += 32) dst[j] = srcr[j];
     }
+  }
+}
+
+// walk adjacency (wv_walk_adjacency_build): per edge e of the packed CSR,
+// {pred, dst, row start of dst, out-degree of dst}; E < 2^32 (row starts fit u32)
+__global__ void walk_adj_build(const int64_t* __restrict__ off, const uint64_t* __restrict__ edges, int64_t E,
+                               uint4* __restrict__ adj) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t pe = edges[e];
+    const uint32_t dst = (uint32_t)pe;
+    const int64_t lo = off[dst], hi = off[dst + 1];
+    adj[e] = make_uint4((uint32_t)(pe >> 32), dst, (uint32_t)lo, (uint32_t)(hi - lo));
   }
 }
 
@@ -418,7 +481,21 @@ static inline int64_t al256(int64_t b) { return (b + 255) & ~(int64_t)255; }
 
 extern "C" {
 
-int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
+int wv_walk_adjacency_build(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
+                            int64_t edge_count, void* walk_adj, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(edge_count >= 0 && edge_count < (1ll << 32), "walk adjacency needs fewer than 2^32 edges");
+  WV_CHECK_ARG(vertex_count < (1ll << 32), "walk adjacency needs fewer than 2^32 vertices");
+  if (edge_count == 0) return 0;
+  const int64_t g = (edge_count + 255) / 256;
+  walk_adj_build<<<(unsigned)(g < 148 * 32 ? g : 148 * 32), 256, 0, (cudaStream_t)stream>>>(
+      row_offsets, packed_edges, edge_count, (uint4*)walk_adj);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
+int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, const void* walk_adj,
+                    int64_t vertex_count,
                     const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth,
                     int64_t work_begin, int64_t work_count, const uint32_t* seed_prefix, int n_prefix, int rng_kind,
                     int32_t* corpus, int32_t* lengths, void* stream) {
@@ -440,6 +517,7 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, in
   WalkParams P;
   P.row_offsets = row_offsets;
   P.edges = packed_edges;
+  P.adj = (const uint4*)walk_adj;
   P.roots = roots;
   P.walk_number = walk_number;
   P.inv_walk_number = 1.0 / (double)walk_number;

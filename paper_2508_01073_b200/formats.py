@@ -140,3 +140,34 @@ def load_corpus_binary(path):
     if n_tok and int(tokens[:n_tok].min()) < 0:
         raise ValueError("token out of int32 range")
     return WalkCorpus.from_device(tokens, offsets, count, n_tok, strategies[strategy_b], projections[projection_b])
+
+
+def save_vocabulary_tsv(vocab, path):
+    """Vocabulary.save_tsv (ingest.py:307-323) with the lines formatted on the device:
+    token, escaped lexical (_escape_field, ingest.py:345-346), roles, frequency."""
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lexicals = list(vocab.lexical_of)
+    rows = len(lexicals)
+    enc = [s_.encode("utf-8", "surrogatepass") for s_ in lexicals]
+    lex_off = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(np.fromiter((len(b) for b in enc), dtype=np.int64, count=rows), out=lex_off[1:])
+    ents, preds = vocab._entity_tokens, vocab._predicate_tokens
+    roles = np.fromiter(((1 if t in ents else 0) | (2 if t in preds else 0) for t in range(rows)), dtype=np.uint8,
+                        count=rows)
+    freq = vocab.frequency
+    counts = np.zeros(rows, dtype=np.int64) if freq is None else np.asarray(freq, dtype=np.int64)[:rows]
+    d_lex = torch.frombuffer(bytearray(b"".join(enc) or b"\0"), dtype=torch.uint8).to(dev)
+    d_off = torch.from_numpy(lex_off).to(dev)
+    d_roles = torch.from_numpy(roles if rows else np.zeros(1, np.uint8)).to(dev)
+    d_counts = torch.from_numpy(counts if rows else np.zeros(1, np.int64)).to(dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(_lib.query("wv_vocab_tsv_workspace_bytes", rows), dtype=torch.uint8, device=dev)
+    st = _lib.stream_ptr()
+    args = (_lib.ptr(d_lex), _lib.ptr(d_off), rows, _lib.ptr(d_roles), _lib.ptr(d_counts))
+    _lib.call("wv_vocab_tsv", *args, None, _lib.ptr(total), _lib.ptr(ws), ws.numel(), st)
+    n = int(total.item())
+    out = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    _lib.call("wv_vocab_tsv", *args, _lib.ptr(out), _lib.ptr(total), _lib.ptr(ws), ws.numel(), st)
+    with open(path, "wb") as fh:
+        fh.write(out[:n].cpu().numpy().tobytes())

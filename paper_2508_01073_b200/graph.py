@@ -24,6 +24,24 @@ class Graph:
         self.d_row_offsets = d_row_offsets  # torch int64 [V+1] (cuda)
         self.d_edges = d_edges  # torch int64 [E] holding u64 (pred << 32 | dst)
         self._np = {}
+        self._adj = None
+
+    def walk_adjacency(self):
+        """Device [E, 4] int32 {pred, dst, row start of dst, out-degree of dst} (built once, cached):
+        a walk hop reads one 16-byte entry instead of offsets then edge.  None when E >= 2^32
+        or WV_NO_WALK_ADJ is set (the walks then read the CSR directly)."""
+        import os
+
+        if self._adj is None:
+            if self.edge_count == 0 or self.edge_count >= (1 << 32) or self.vertex_count >= (1 << 32) or \
+                    os.environ.get("WV_NO_WALK_ADJ"):
+                return None
+            torch = _lib.require_cuda()
+            adj = torch.empty((self.edge_count, 4), dtype=torch.int32, device=self.d_edges.device)
+            _lib.call("wv_walk_adjacency_build", _lib.ptr(self.d_row_offsets), _lib.ptr(self.d_edges),
+                      self.vertex_count, self.edge_count, _lib.ptr(adj), _lib.stream_ptr())
+            self._adj = adj
+        return self._adj
 
     # -- reference-compatible views -------------------------------------
     def _unpacked(self):

@@ -16,6 +16,7 @@ from __future__ import annotations
 import importlib
 
 _saved: dict = {}
+_saved_methods: dict = {}
 
 
 def _wrap_train(train_fn, precision: str, pairs: str, package: str):
@@ -107,9 +108,16 @@ def install(package: str = "walkvec", *, precision: str = "fp64", pairs: str = "
     for mod, name, fn in targets:
         _saved.setdefault((mod.__name__, name), getattr(mod, name))
         setattr(mod, name, fn)
+    # Vocabulary.save_tsv is a method (cli.py:116, pipeline.py:302): swap it on the class
+    ingest_mod = importlib.import_module(f"{package}.ingest")
+    _saved_methods.setdefault((ingest_mod.__name__, "Vocabulary", "save_tsv"), ingest_mod.Vocabulary.save_tsv)
+    ingest_mod.Vocabulary.save_tsv = lambda self, path: dev_formats.save_vocabulary_tsv(self, path)
 
 
 def uninstall():
     for (modname, name), fn in list(_saved.items()):
         setattr(importlib.import_module(modname), name, fn)
     _saved.clear()
+    for (modname, cls, name), fn in list(_saved_methods.items()):
+        setattr(getattr(importlib.import_module(modname), cls), name, fn)
+    _saved_methods.clear()

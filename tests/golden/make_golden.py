@@ -335,6 +335,23 @@ def formats():
     rw.save_corpus_binary(corpus, path)
     out["wvc1"] = base64.b64encode(open(path, "rb").read()).decode()
     out["wvc1_tokens"], out["wvc1_offsets"] = toks.tolist(), offs
+    # Vocabulary.save_tsv (ingest.py:307-323): escaped lexicals, roles, frequencies
+    from walkvec.ingest import Vocabulary
+
+    voc = Vocabulary()
+    lexs = ["http://a/0", "tab\there", "new\nline", "back\\slash", "cr\rx", "é ü 漢", "", "p:knows", "plain"]
+    for i, lx in enumerate(lexs):
+        (voc._intern_predicate if i in (1, 7) else voc._intern_entity)(lx)
+    voc._intern_predicate("plain")  # entity and predicate
+    voc.frequency = np.array([3, 0, 7, 12, 1, 0, 5, 100, 2], dtype=np.int64)
+    with tempfile.NamedTemporaryFile(delete=False) as fh:
+        path = fh.name
+    voc.save_tsv(path)
+    out["vocab_tsv"] = base64.b64encode(open(path, "rb").read()).decode()
+    out["vocab_lexicals"] = lexs
+    out["vocab_entities"] = sorted(voc._entity_tokens)
+    out["vocab_predicates"] = sorted(voc._predicate_tokens)
+    out["vocab_frequency"] = voc.frequency.tolist()
     (OUT / "formats.json").write_text(json.dumps(out, ensure_ascii=False) + "\n")
 
 

@@ -124,3 +124,18 @@ def test_wvc1_reader_errors(tmp_path):
     p.write_bytes(_wvc1_bytes([[1, 2], [3]], count=3))  # fewer records than the header says
     with pytest.raises(IndexError):
         formats.load_corpus_binary(p)
+
+
+def test_vocabulary_tsv_byte_exact(tmp_path):
+    """Vocabulary.save_tsv's bytes (reference output in tests/golden/formats.json): escaped
+    tabs / newlines / backslashes / CR, UTF-8, an empty lexical, roles e / p / ep, frequencies."""
+    from paper_2508_01073_b200 import formats
+
+    class Voc:
+        lexical_of = G["vocab_lexicals"]
+        _entity_tokens = set(G["vocab_entities"])
+        _predicate_tokens = set(G["vocab_predicates"])
+        frequency = np.array(G["vocab_frequency"])
+
+    formats.save_vocabulary_tsv(Voc(), tmp_path / "v.tsv")
+    assert (tmp_path / "v.tsv").read_bytes() == base64.b64decode(G["vocab_tsv"])

@@ -145,3 +145,18 @@ def test_barabasi_bit_exact_vs_oracle(wv, n, m, seed):
     oe, oV, oent, oprd = osy.barabasi_kg(n, m, 12, seed)
     assert V == oV and np.array_equal(e.cpu().numpy(), oe)
     assert np.array_equal(ent.cpu().numpy(), oent) and np.array_equal(prd.cpu().numpy(), oprd)
+
+
+def test_device_encode_matches_reference_vocabulary(wv, golden):
+    """wv_encode_triples on the reference's own BA edges and predicate picks equals the
+    reference's build_vocabulary encoding (tests/golden/vocab.npz, ingest.py:368-396)."""
+    import torch
+
+    from paper_2508_01073_b200 import synth
+
+    g = golden("vocab.npz")
+    raw = torch.from_numpy(g["raw"]).cuda()
+    picks = torch.from_numpy(g["picks"]).cuda()
+    e, V, ent, _ = synth.device_encode(raw[:, 0].contiguous(), picks, raw[:, 1].contiguous(), 300, 5)
+    assert V == int(g["V"]) and np.array_equal(e.cpu().numpy(), g["edges"])
+    assert np.array_equal(ent.cpu().numpy(), g["entity_tokens"])

@@ -211,3 +211,22 @@ def test_cfg4_er_long_walks_shards_bit_exact(wv):
         w0 = s * ow.SHARD
         lo, hi = c.offsets[w0], c.offsets[min(w0 + ow.SHARD, len(c))]
         assert np.array_equal(c.tokens[lo:hi], tok)
+
+
+@pytest.mark.parametrize("rng", ["pcg64", "philox"])
+def test_walk_adjacency_path_equals_csr_path(rng, monkeypatch):
+    """The one-load-per-hop walk adjacency ({pred, dst, row start, degree} per edge) gives the
+    same corpus as the offsets -> edge CSR path, dead ends (the BA DAG's sinks) included."""
+    import paper_2508_01073_b200 as wv
+    from paper_2508_01073_b200.synth import synthetic_kg
+
+    edges, V, ents, _ = synthetic_kg("barabasi", 20_000, m=3, predicates=9, seed=11)
+    g = wv.build_graph(edges, V)
+    a = wv.random_walks(g, ents, walk_depth=7, walk_number=6, rng_seed=5, rng=rng)
+    assert g.walk_adjacency() is not None
+    monkeypatch.setenv("WV_NO_WALK_ADJ", "1")
+    g2 = wv.build_graph(edges, V)
+    assert g2.walk_adjacency() is None
+    b = wv.random_walks(g2, ents, walk_depth=7, walk_number=6, rng_seed=5, rng=rng)
+    assert np.array_equal(a.tokens, b.tokens) and np.array_equal(a.offsets, b.offsets)
+    assert (np.diff(a.offsets) < 15).any()  # some walks end early at a sink

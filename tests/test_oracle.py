@@ -185,3 +185,15 @@ def test_synth_oracle_mulhi_and_philox():
     assert [int(x[0]) for x in c] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
     c = osy.philox4x32_10([0xFFFFFFFF] * 1, [0xFFFFFFFF], [0xFFFFFFFF], [0xFFFFFFFF], 0xFFFFFFFF, 0xFFFFFFFF)
     assert [int(x[0]) for x in c] == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+
+
+def test_synth_encoding_matches_reference_vocabulary(golden):
+    """oracle/synth.encode on the reference's own BA edges and predicate picks reproduces the
+    reference's build_vocabulary encoding (tests/golden/vocab.npz, ingest.py:368-396)."""
+    from oracle import synth as osy
+
+    g = golden("vocab.npz")
+    raw = g["raw"]
+    edges, V, ent, _ = osy.encode(raw[:, 0], g["picks"], raw[:, 1], 300)
+    assert np.array_equal(edges, g["edges"]) and V == int(g["V"])
+    assert np.array_equal(ent, g["entity_tokens"])
