@@ -538,7 +538,7 @@ int wv_vocab_tsv(const uint8_t* lex, const int64_t* lex_off, int64_t rows, const
   const unsigned g = (unsigned)((rows + 255) / 256 < 148 * 16 ? (rows + 255) / 256 : 148 * 16);
   vtsv_len<<<g, 256, 0, st>>>(lex, lex_off, rows, roles, counts, line);
   WV_LAUNCH_CHECK();
-  WV_CUDA(excl_scan<int64_t, int64_t>(line, rows, line, total, sws, st));
+  WV_CUDA((excl_scan<int64_t, int64_t>(line, rows, line, total, sws, st)));
   if (out != nullptr) {
     vtsv_emit<<<g, 256, 0, st>>>(lex, lex_off, rows, roles, counts, line, out);
     WV_LAUNCH_CHECK();
