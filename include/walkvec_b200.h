@@ -90,10 +90,12 @@ int wv_csr_unpack(const uint64_t* packed_edges, int64_t E, int64_t* col_targets,
  * 8-byte CSR reads cost a 64-byte DRAM fetch each (ncu: 113 B/hop at cfg5). */
 int wv_walk_adjacency_build(const int64_t* row_offsets, const uint64_t* packed_edges, int64_t vertex_count,
                             int64_t edge_count, void* walk_adj, void* stream);
+/* workspace: the launch's per-shard generator seeds (ws = NULL seeds per CTA) */
+int64_t wv_random_walks_workspace_bytes(int64_t work_begin, int64_t work_count);
 int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, const void* walk_adj,
                     int64_t vertex_count, const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth, int64_t work_begin,
                     int64_t work_count, const uint32_t* seed_prefix, int n_prefix, int rng_kind, int32_t* corpus,
-                    int32_t* lengths, void* stream);
+                    int32_t* lengths, void* ws, int64_t ws_bytes, void* stream);
 
 /* fixed-width rows -> flat tokens (int32 or int64 by token_bytes) + int64 offsets[n+1]
  * (the PAD strip + concatenate + cumsum of walks.py:139-141, 181-184) */

@@ -130,7 +130,8 @@ SIGNATURES = {
     "wv_csr_build": (I32, [P, I64, I64, P, P, P, I64, P]),
     "wv_csr_unpack": (I32, [P, I64, P, P, P]),
     "wv_walk_adjacency_build": (I32, [P, P, I64, I64, P, P]),
-    "wv_random_walks": (I32, [P, P, P, I64, P, I64, I64, I32, I64, I64, P, I32, I32, P, P, P]),
+    "wv_random_walks_workspace_bytes": (I64, [I64, I64]),
+    "wv_random_walks": (I32, [P, P, P, I64, P, I64, I64, I32, I64, I64, P, I32, I32, P, P, P, I64, P]),
     "wv_compact_workspace_bytes": (I64, [I64]),
     "wv_corpus_compact": (I32, [P, P, I64, I32, P, P, I32, P, I64, P]),
     "wv_dedup_workspace_bytes": (I64, [I64]),

@@ -494,11 +494,18 @@ int wv_walk_adjacency_build(const int64_t* row_offsets, const uint64_t* packed_e
   return 0;
 }
 
+int64_t wv_random_walks_workspace_bytes(int64_t work_begin, int64_t work_count) {
+  using namespace wv;
+  if (work_count <= 0) return 256;
+  const int64_t n_seeds = (work_begin + work_count - 1) / kShard - work_begin / kShard + 1;
+  return n_seeds * 32 + 256;
+}
+
 int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, const void* walk_adj,
                     int64_t vertex_count,
                     const int64_t* roots, int64_t n_roots, int64_t walk_number, int walk_depth,
                     int64_t work_begin, int64_t work_count, const uint32_t* seed_prefix, int n_prefix, int rng_kind,
-                    int32_t* corpus, int32_t* lengths, void* stream) {
+                    int32_t* corpus, int32_t* lengths, void* ws, int64_t ws_bytes, void* stream) {
   using namespace wv;
   WV_CHECK_ARG(walk_depth >= 1, "walk_depth must be >= 1");
   WV_CHECK_ARG(walk_number >= 1, "walk_number must be >= 1");
@@ -547,9 +554,9 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, co
   uint64_t* seeds = nullptr;
   const int64_t s_first = work_begin / kShard;
   const int64_t n_seeds = work_count > 0 ? (work_begin + work_count - 1) / kShard - s_first + 1 : 0;
-  if (WV_WALK_SEED_TABLE && n_seeds > 0) {
-    // stream-ordered scratch (freed after the walk kernel on the same stream)
-    WV_CUDA(cudaMallocAsync((void**)&seeds, (size_t)n_seeds * 32, st));
+  if (WV_WALK_SEED_TABLE && n_seeds > 0 && ws != nullptr) {
+    WV_CHECK_ARG(ws_bytes >= wv_random_walks_workspace_bytes(work_begin, work_count), "workspace too small");
+    seeds = (uint64_t*)ws;  // per-shard seeds in the caller's workspace (ws = NULL: seeded per CTA)
     if (rng_kind == WV_RNG_PCG64)
       seed_shards<WV_RNG_PCG64><<<(unsigned)((n_seeds + 127) / 128), 128, 0, st>>>(P, s_first, n_seeds, seeds);
     else
@@ -569,7 +576,6 @@ int wv_random_walks(const int64_t* row_offsets, const uint64_t* packed_edges, co
     rc = two ? launch(random_walk_kernel<WV_RNG_PHILOX, 2>) : launch(random_walk_kernel<WV_RNG_PHILOX, 1>);
   if (rc) return rc;
   WV_LAUNCH_CHECK();
-  if (seeds) WV_CUDA(cudaFreeAsync(seeds, st));
   return 0;
 }
 

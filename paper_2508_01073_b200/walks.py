@@ -192,10 +192,10 @@ def random_walks_fixed(graph, roots, walk_depth: int, walk_number: int, rng_seed
     lengths = torch.empty(max(work_count, 1), dtype=torch.int32, device=dev)
     words, n = words_array(entropy_words([rng_seed, 0]))
     adj = g.walk_adjacency()
+    ws = _ws(torch, _lib.query("wv_random_walks_workspace_bytes", int(work_begin), int(work_count)), dev)
     _lib.call("wv_random_walks", _lib.ptr(g.d_row_offsets), _lib.ptr(g.d_edges), _lib.ptr(adj), g.vertex_count,
-              _lib.ptr(roots),
-              n_roots, int(walk_number), int(walk_depth), int(work_begin), int(work_count), words, n,
-              _RNG_KINDS[rng], _lib.ptr(corpus), _lib.ptr(lengths), _lib.stream_ptr())
+              _lib.ptr(roots), n_roots, int(walk_number), int(walk_depth), int(work_begin), int(work_count), words, n,
+              _RNG_KINDS[rng], _lib.ptr(corpus), _lib.ptr(lengths), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     return corpus, lengths, width
 
 
