@@ -322,8 +322,18 @@ int64_t wv_ingest_lines_workspace_bytes(int64_t n_bytes);
 int wv_ingest_lines(const uint8_t* text, int64_t n_bytes, int64_t* line_end, int64_t* n_terms, void* ws,
                     int64_t ws_bytes, void* stream);
 int64_t wv_ingest_workspace_bytes(int64_t n_lines);
+/* csv.reader records of a quoted csv/tsv text (quoted fields may hold the
+ * delimiter and line breaks): rec_end[r] = position of record r's terminator,
+ * rec_line[r] = csv.reader's line_num after it; *n_records, *n_lines (device)
+ * = terminated records, universal-newline line terminators.  Parse them with
+ * wv_ingest_parse mode 3, line_end = rec_end, line_no = rec_line. */
+int64_t wv_ingest_records_workspace_bytes(int64_t n_bytes);
+int wv_ingest_records(const uint8_t* text, int64_t n_bytes, int delim, int64_t* rec_end, int64_t* rec_line,
+                      int64_t* n_records, int64_t* n_lines, void* ws, int64_t ws_bytes, void* stream);
+/* mode 3: quoted delimiter table over csv.reader records; line_no (mode 3) = each
+ * record's line number (has_header skips the record at line 1); NULL otherwise */
 int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_end, int64_t n_lines, int mode,
-                    uint64_t hash_seed, int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
+                    const int64_t* line_no, uint64_t hash_seed, int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
                     int64_t* bad, int64_t* n_out, int64_t* edges, uint32_t* roles, int64_t* tok_span, void* ws,
                     int64_t ws_bytes, void* stream);
 

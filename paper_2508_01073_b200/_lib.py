@@ -176,7 +176,9 @@ SIGNATURES = {
     "wv_ingest_lines_workspace_bytes": (I64, [I64]),
     "wv_ingest_lines": (I32, [P, I64, P, P, P, I64, P]),
     "wv_ingest_workspace_bytes": (I64, [I64]),
-    "wv_ingest_parse": (I32, [P, I64, P, I64, I32, C.c_uint64, I32, I32, I32, P, P, P, P, P, P, P, P, P, I64, P]),
+    "wv_ingest_records_workspace_bytes": (I64, [I64]),
+    "wv_ingest_records": (I32, [P, I64, I32, P, P, P, P, P, I64, P]),
+    "wv_ingest_parse": (I32, [P, I64, P, I64, I32, P, C.c_uint64, I32, I32, I32, P, P, P, P, P, P, P, P, P, I64, P]),
     "wv_shard_init": (I32, [I64, I32, P, I32, I32, I32, I32, P, P, P]),
     "wv_shard_decode_group": (I32, [P, P, P, I64, I64, I32, I32, P]),
     "wv_shard_requests": (I32, [P, P, P, I64, I64, I32, I32, I64, I64, P, P, P, P, P, P]),

@@ -41,18 +41,42 @@ __device__ __forceinline__ int hexval(uint8_t c) {
 
 // Unescaped byte stream of a raw span (escapes decoded, code points re-encoded
 // as UTF-8, lone surrogates with the generic 3-byte form).
+// mode: 0 raw bytes; 1 N-Triples escapes; 2 a csv.reader quoted field (opening
+// quote skipped, "" -> ", characters after the closing quote kept literally)
 struct KeyIter {
   const uint8_t* p;
   const uint8_t* e;
-  bool esc;
+  uint8_t esc;
+  uint8_t qs;  // csv: 0 before the opening quote, 1 inside the quotes, 2 after the closing quote
   uint8_t buf[4];
   int nb, ib;
-  __device__ KeyIter(const uint8_t* text, int64_t s, int64_t t, bool escaped)
-      : p(text + s), e(text + t), esc(escaped), nb(0), ib(0) {}
+  __device__ KeyIter(const uint8_t* text, int64_t s, int64_t t, uint8_t mode)
+      : p(text + s), e(text + t), esc(mode), qs(0), nb(0), ib(0) {}
   __device__ bool next(uint8_t& out) {
     if (ib < nb) {
       out = buf[ib++];
       return true;
+    }
+    if (esc == 2) {
+      while (p < e) {
+        const uint8_t c = *p++;
+        if (qs == 0) {  // the opening quote
+          qs = 1;
+          continue;
+        }
+        if (qs == 1 && c == '"') {
+          if (p < e && *p == '"') {  // doubled quote
+            ++p;
+            out = '"';
+            return true;
+          }
+          qs = 2;  // closing quote
+          continue;
+        }
+        out = c;
+        return true;
+      }
+      return false;
     }
     if (p >= e) return false;
     const uint8_t c = *p;
@@ -105,7 +129,7 @@ struct KeyIter {
   }
 };
 
-__device__ uint64_t key_hash(const uint8_t* text, int64_t s, int64_t t, bool esc, uint64_t seed) {
+__device__ uint64_t key_hash(const uint8_t* text, int64_t s, int64_t t, uint8_t esc, uint64_t seed) {
   KeyIter it(text, s, t, esc);
   uint64_t h = 0xcbf29ce484222325ull ^ (seed ? splitmix64(seed) : 0ull);
   uint64_t n = 0;
@@ -118,7 +142,8 @@ __device__ uint64_t key_hash(const uint8_t* text, int64_t s, int64_t t, bool esc
   return h ? h : 1ull;  // 0 marks an empty table slot
 }
 
-__device__ bool key_equal(const uint8_t* text, int64_t s1, int64_t t1, bool e1, int64_t s2, int64_t t2, bool e2) {
+__device__ bool key_equal(const uint8_t* text, int64_t s1, int64_t t1, uint8_t e1, int64_t s2, int64_t t2,
+                          uint8_t e2) {
   if (!e1 && !e2) {
     if (t1 - s1 != t2 - s2) return false;
     for (int64_t i = 0; i < t1 - s1; ++i)
@@ -278,10 +303,90 @@ __global__ void ingest_line_bounds(const uint8_t* __restrict__ term, const int64
     if (term[i]) line_end[pos[i]] = i;
 }
 
+// ------------------------------------------------------ csv.reader records --
+// Quoted csv/tsv fields may hold delimiters and line breaks, so a record is not a
+// line.  csv.reader's quoting (excel dialect, strict=False) as a per-byte state
+// machine: 0 start of field, 1 unquoted field, 2 quoted field, 3 quote seen in a
+// quoted field.  A '\n' / lone '\r' / the '\n' of "\r\n" ends a record unless the
+// state before it is 2.  The states entering each 4 KB chunk come from composing
+// per-chunk transition maps (4 states -> 4 states).
+constexpr int64_t kCsvChunk = 4096;
+
+__device__ __forceinline__ uint8_t csv_step(uint8_t st, uint8_t c, uint8_t delim) {
+  if (c == '"') return st == 0 ? 2 : (st == 1 ? 1 : (st == 2 ? 3 : 2));
+  if (c == delim || c == '\n' || c == '\r') return st == 2 ? 2 : 0;
+  return st == 2 ? 2 : 1;
+}
+
+__global__ void csv_chunk_maps(const uint8_t* __restrict__ text, int64_t n, uint8_t delim, int64_t n_chunks,
+                               uint8_t* __restrict__ maps) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_chunks * 4) return;
+  const int64_t c = t >> 2;
+  uint8_t st = (uint8_t)(t & 3);
+  const int64_t e = min(n, (c + 1) * kCsvChunk);
+  for (int64_t i = c * kCsvChunk; i < e; ++i) st = csv_step(st, text[i], delim);
+  maps[t] = st;
+}
+
+// one block: the state entering every chunk (thread ranges composed, then resolved in order)
+__global__ void __launch_bounds__(1024) csv_chunk_states(const uint8_t* __restrict__ maps, int64_t n_chunks,
+                                                         uint8_t* __restrict__ start) {
+  __shared__ uint8_t f[1024][4];
+  __shared__ uint8_t entry[1024];
+  const int64_t per = (n_chunks + 1023) / 1024;
+  const int64_t c0 = threadIdx.x * per, c1 = min(n_chunks, c0 + per);
+  uint8_t g[4] = {0, 1, 2, 3};
+  for (int64_t c = c0; c < c1; ++c)
+    for (int s = 0; s < 4; ++s) g[s] = maps[4 * c + g[s]];
+  for (int s = 0; s < 4; ++s) f[threadIdx.x][s] = g[s];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint8_t st = 0;
+    for (int j = 0; j < 1024; ++j) {
+      entry[j] = st;
+      st = f[j][st];
+    }
+  }
+  __syncthreads();
+  uint8_t st = entry[threadIdx.x];
+  for (int64_t c = c0; c < c1; ++c) {
+    start[c] = st;
+    st = maps[4 * c + st];
+  }
+}
+
+// record terminators (rec) and universal-newline line terminators (phys)
+__global__ void csv_terms(const uint8_t* __restrict__ text, int64_t n, uint8_t delim, int64_t n_chunks,
+                          const uint8_t* __restrict__ start, uint8_t* __restrict__ rec, uint8_t* __restrict__ phys) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks; c += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t st = start[c];
+    const int64_t e = min(n, (c + 1) * kCsvChunk);
+    for (int64_t i = c * kCsvChunk; i < e; ++i) {
+      const uint8_t ch = text[i];
+      const bool term = ch == '\n' || (ch == '\r' && (i + 1 == n || text[i + 1] != '\n'));
+      phys[i] = term ? 1 : 0;
+      rec[i] = (term && st != 2) ? 1 : 0;
+      st = csv_step(st, ch, delim);
+    }
+  }
+}
+
+__global__ void csv_record_bounds(const uint8_t* __restrict__ rec, const int64_t* __restrict__ rpos,
+                                  const int64_t* __restrict__ ppos, int64_t n, int64_t* __restrict__ rec_end,
+                                  int64_t* __restrict__ rec_line) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (rec[i]) {
+      rec_end[rpos[i]] = i;
+      rec_line[rpos[i]] = ppos[i] + 1;  // csv.reader's line_num after the record
+    }
+}
+
 // Per line: status, error (code, byte position) and the three key spans.
 // mode: 0 N-Triples; 1 whitespace table; 2 delimiter table (delim)
 __global__ void ingest_parse(const uint8_t* __restrict__ text, int64_t n, const int64_t* __restrict__ line_end,
-                             int64_t n_lines, int mode, uint8_t delim, int has_header, uint8_t* __restrict__ status,
+                             int64_t n_lines, int mode, uint8_t delim, int has_header,
+                             const int64_t* __restrict__ line_no, uint8_t* __restrict__ status,
                              int32_t* __restrict__ err, int64_t* __restrict__ err_at, Term* __restrict__ terms) {
   for (int64_t L = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; L < n_lines;
        L += (int64_t)gridDim.x * blockDim.x) {
@@ -328,8 +433,9 @@ __global__ void ingest_parse(const uint8_t* __restrict__ text, int64_t n, const 
       err_at[L] = at;
       continue;
     }
-    // tables: every non-empty row becomes a resource triple (exactly 3 columns)
-    if (has_header && L == 0) continue;
+    // tables: every non-empty row becomes a resource triple (exactly 3 columns);
+    // the header is the row csv.reader reports at line 1
+    if (has_header && (line_no ? line_no[L] == 1 : L == 0)) continue;
     int cols = 0;
     int64_t i = b;
     bool quoted = false;
@@ -342,7 +448,7 @@ __global__ void ingest_parse(const uint8_t* __restrict__ text, int64_t n, const 
         if (cols < 3) tm[cols] = Term{s, i, TK_IRI, 0};
         ++cols;
       }
-    } else {
+    } else if (mode == 2) {
       if (e == b) continue;  // csv.reader yields [] for an empty row
       int64_t s = b;
       for (i = b; i <= e; ++i) {
@@ -353,11 +459,30 @@ __global__ void ingest_parse(const uint8_t* __restrict__ text, int64_t n, const 
           s = i + 1;
         }
       }
+    } else {  // mode 3: a csv.reader record with quoting (the record may span lines)
+      if (e == b) continue;
+      int64_t s = b;
+      uint8_t st = 0;
+      for (i = b; i <= e; ++i) {
+        if (i == e || (text[i] == delim && st != 2)) {
+          const uint8_t q = (i > s && text[s] == '"') ? 2 : 0;  // a field opened by a quote
+          if (cols < 3) tm[cols] = Term{s, i, TK_IRI, q};
+          ++cols;
+          s = i + 1;
+          st = 0;
+          continue;
+        }
+        st = csv_step(st, text[i], delim);
+      }
     }
     if (cols == 0) continue;
     int code = cols == 3 ? E_NONE : E_COLUMNS;
     if (mode == 2 && quoted) code = E_QUOTED;
-    if (!code && (tm[0].t == tm[0].s || tm[1].t == tm[1].s)) code = E_EMPTY_SP;
+    // an empty key: an empty span, or (quoted) exactly the two quotes
+    auto empty_key = [&](const Term& x) {
+      return x.t == x.s || (x.esc == 2 && x.t - x.s == 2 && text[x.s + 1] == '"');
+    };
+    if (!code && (empty_key(tm[0]) || empty_key(tm[1]))) code = E_EMPTY_SP;
     status[L] = code == E_NONE ? LN_OK : (code == E_EMPTY_SP ? LN_VALUE_ERR : LN_PARSE_ERR);
     err[L] = code == E_COLUMNS ? -cols : code;
     err_at[L] = b;
@@ -453,7 +578,7 @@ __global__ void ingest_rank(const uint32_t* __restrict__ firsts, const uint32_t*
     const Term tm = occ[firsts[r]];
     tok_span[3 * r] = tm.s;
     tok_span[3 * r + 1] = tm.t;
-    tok_span[3 * r + 2] = (int64_t)tm.esc | ((int64_t)tm.kind << 1);
+    tok_span[3 * r + 2] = (int64_t)tm.esc | ((int64_t)tm.kind << 2);
   }
 }
 
@@ -542,14 +667,57 @@ int64_t wv_ingest_workspace_bytes(int64_t n_lines) {
          a256(radix_ws_bytes(occ, 32)) + a256(16) + 1024;
 }
 
+int64_t wv_ingest_records_workspace_bytes(int64_t n_bytes) {
+  using namespace wv;
+  const int64_t chunks = (n_bytes + kCsvChunk - 1) / kCsvChunk;
+  return 2 * a256(n_bytes) + 2 * a256((n_bytes + 1) * 8) + 2 * a256(scan_tiles(n_bytes) * 8) + a256(chunks * 4) +
+         a256(chunks) + 1024;
+}
+
+int wv_ingest_records(const uint8_t* text, int64_t n_bytes, int delim, int64_t* rec_end, int64_t* rec_line,
+                      int64_t* n_records, int64_t* n_lines, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace wv;
+  WV_CHECK_ARG(n_bytes >= 1, "empty input");
+  WV_CHECK_ARG(ws_bytes >= wv_ingest_records_workspace_bytes(n_bytes), "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t chunks = (n_bytes + kCsvChunk - 1) / kCsvChunk;
+  char* w = (char*)ws;
+  uint8_t* rec = (uint8_t*)w;
+  w += a256(n_bytes);
+  uint8_t* phys = (uint8_t*)w;
+  w += a256(n_bytes);
+  int64_t* rpos = (int64_t*)w;
+  w += a256((n_bytes + 1) * 8);
+  int64_t* ppos = (int64_t*)w;
+  w += a256((n_bytes + 1) * 8);
+  int64_t* sws1 = (int64_t*)w;
+  w += a256(scan_tiles(n_bytes) * 8);
+  int64_t* sws2 = (int64_t*)w;
+  w += a256(scan_tiles(n_bytes) * 8);
+  uint8_t* maps = (uint8_t*)w;
+  w += a256(chunks * 4);
+  uint8_t* start = (uint8_t*)w;
+  csv_chunk_maps<<<gridn(chunks * 4, 256), 256, 0, st>>>(text, n_bytes, (uint8_t)delim, chunks, maps);
+  WV_LAUNCH_CHECK();
+  csv_chunk_states<<<1, 1024, 0, st>>>(maps, chunks, start);
+  WV_LAUNCH_CHECK();
+  csv_terms<<<gridn(chunks, 128), 128, 0, st>>>(text, n_bytes, (uint8_t)delim, chunks, start, rec, phys);
+  WV_LAUNCH_CHECK();
+  WV_CUDA((excl_scan<uint8_t, int64_t>(rec, n_bytes, rpos, n_records, sws1, st)));
+  WV_CUDA((excl_scan<uint8_t, int64_t>(phys, n_bytes, ppos, n_lines, sws2, st)));
+  csv_record_bounds<<<gridn(n_bytes, 256), 256, 0, st>>>(rec, rpos, ppos, n_bytes, rec_end, rec_line);
+  WV_LAUNCH_CHECK();
+  return 0;
+}
+
 int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_end, int64_t n_lines, int mode,
-                    uint64_t hash_seed,
+                    const int64_t* line_no, uint64_t hash_seed,
                     int delim, int has_header, int include_literals, uint8_t* status, int32_t* err, int64_t* err_at,
                     int64_t* bad, int64_t* n_out, int64_t* edges, uint32_t* roles, int64_t* tok_span, void* ws,
                     int64_t ws_bytes, void* stream) {
   using namespace wv;
   WV_CHECK_ARG(n_lines >= 1, "empty input");
-  WV_CHECK_ARG(mode >= 0 && mode <= 2, "bad mode");
+  WV_CHECK_ARG(mode >= 0 && mode <= 3, "bad mode");
   WV_CHECK_ARG(3 * n_lines < (int64_t)0xffffffffLL, "input too large for 32-bit positions");
   WV_CHECK_ARG(ws_bytes >= wv_ingest_workspace_bytes(n_lines), "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
@@ -581,7 +749,7 @@ int wv_ingest_parse(const uint8_t* text, int64_t n_bytes, const int64_t* line_en
   void* rws = take(radix_ws_bytes(n_occ_max, 32));
 
   ingest_parse<<<gridn(n_lines, 128), 128, 0, st>>>(text, n_bytes, line_end, n_lines, mode, (uint8_t)delim,
-                                                    has_header, status, err, err_at, terms);
+                                                    has_header, line_no, status, err, err_at, terms);
   WV_LAUNCH_CHECK();
   const int64_t big[2] = {INT64_MAX, INT64_MAX};
   WV_CUDA(cudaMemcpyAsync(bad, big, 16, cudaMemcpyHostToDevice, st));

@@ -145,6 +145,25 @@ _MESSAGES = {
 _STRING_ESCAPES = {"t": "\t", "b": "\b", "n": "\n", "r": "\r", "f": "\f", '"': '"', "'": "'", "\\": "\\"}
 
 
+def _csv_unquote(raw: str) -> str:
+    """A csv.reader quoted field's value from its raw text: the opening quote dropped, "" -> ",
+    text after the closing quote kept (excel dialect, strict=False)."""
+    out, i, inside = [], 1, True
+    while i < len(raw):
+        c = raw[i]
+        if inside and c == '"':
+            if i + 1 < len(raw) and raw[i + 1] == '"':
+                out.append('"')
+                i += 2
+                continue
+            inside = False
+            i += 1
+            continue
+        out.append(c)
+        i += 1
+    return "".join(out)
+
+
 def _unescape_key(raw: str) -> str:
     """Decode a key span the device already validated (ingest.py:72-101)."""
     if "\\" not in raw:
@@ -207,8 +226,8 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
     (format "nt") or ``build_vocabulary(parse_edge_table(path, format, has_header))``
     (ingest.py:188-257, 368-396): same tokens, lexical keys, roles, edges and
     errors (ParseError with the reference's message and line; non-strict
-    N-Triples lines go to ``error_sink``).  Input is UTF-8 bytes; quoted csv/tsv
-    fields are not supported on the device (NotImplementedError).
+    N-Triples lines go to ``error_sink``).  Input is UTF-8 bytes; csv/tsv with
+    quoted fields (delimiters and line breaks inside quotes) follow csv.reader.
     """
     from . import _lib
 
@@ -225,13 +244,30 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
     st = _lib.stream_ptr()
     line_end = torch.empty(n + 1, dtype=torch.int64, device=dev)
     n_terms = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = torch.empty(_lib.query("wv_ingest_lines_workspace_bytes", n), dtype=torch.uint8, device=dev)
-    _lib.call("wv_ingest_lines", _lib.ptr(text), n, _lib.ptr(line_end), _lib.ptr(n_terms), _lib.ptr(ws), ws.numel(),
-              st)
-    n_lines = int(n_terms.item())
-    if raw[-1] not in (10, 13):  # unterminated last line ends at the end of the text
-        line_end[n_lines] = n
-        n_lines += 1
+    mode = _MODES[format]
+    line_no = None
+    if format in ("csv", "tsv") and b'"' in raw:
+        # quoted fields (csv.reader, ingest.py:241) may hold delimiters and line breaks:
+        # records located by the quoting state machine, numbered by csv.reader's line_num
+        mode = 3
+        line_no = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        n_phys = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = torch.empty(_lib.query("wv_ingest_records_workspace_bytes", n), dtype=torch.uint8, device=dev)
+        _lib.call("wv_ingest_records", _lib.ptr(text), n, _DELIM[format], _lib.ptr(line_end), _lib.ptr(line_no),
+                  _lib.ptr(n_terms), _lib.ptr(n_phys), _lib.ptr(ws), ws.numel(), st)
+        n_lines = int(n_terms.item())
+        if n_lines == 0 or int(line_end[n_lines - 1]) != n - 1:  # an unterminated last record
+            line_end[n_lines] = n
+            line_no[n_lines] = int(n_phys.item()) + 1
+            n_lines += 1
+    else:
+        ws = torch.empty(_lib.query("wv_ingest_lines_workspace_bytes", n), dtype=torch.uint8, device=dev)
+        _lib.call("wv_ingest_lines", _lib.ptr(text), n, _lib.ptr(line_end), _lib.ptr(n_terms), _lib.ptr(ws),
+                  ws.numel(), st)
+        n_lines = int(n_terms.item())
+        if raw[-1] not in (10, 13):  # unterminated last line ends at the end of the text
+            line_end[n_lines] = n
+            n_lines += 1
     status = torch.empty(n_lines, dtype=torch.uint8, device=dev)
     err = torch.empty(n_lines, dtype=torch.int32, device=dev)
     err_at = torch.empty(n_lines, dtype=torch.int64, device=dev)
@@ -245,7 +281,8 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
         # a 64-bit key-hash collision (distinct keys, equal hashes) is detected, never merged:
         # re-intern with an independently seeded hash
         n_out.zero_()
-        _lib.call("wv_ingest_parse", _lib.ptr(text), n, _lib.ptr(line_end), n_lines, _MODES[format], hash_seed,
+        _lib.call("wv_ingest_parse", _lib.ptr(text), n, _lib.ptr(line_end), n_lines, mode, _lib.ptr(line_no),
+                  hash_seed,
                   _DELIM[format], int(has_header), int(include_literals), _lib.ptr(status), _lib.ptr(err),
                   _lib.ptr(err_at), _lib.ptr(bad), _lib.ptr(n_out), _lib.ptr(edges), _lib.ptr(roles),
                   _lib.ptr(tok_span), _lib.ptr(ws), ws.numel(), st)
@@ -258,12 +295,11 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
         codes = err.cpu().numpy()
         ats = err_at.cpu().numpy()
         stat = status.cpu().numpy()
-        if 19 in set(codes[stat == 2].tolist()):
-            raise NotImplementedError("quoted csv/tsv fields are not supported by the GPU ingest")
         if format != "nt" or strict:
             if stat[first_bad] == 3:
                 raise ValueError("subject and predicate must be non-empty")
-            raise ParseError(_message(int(codes[first_bad]), raw, int(ats[first_bad])), first_bad + 1)
+            row = int(line_no[first_bad]) if line_no is not None else first_bad + 1
+            raise ParseError(_message(int(codes[first_bad]), raw, int(ats[first_bad])), row)
         stop = first_value if first_value != big else n_lines
         if error_sink is not None:
             for L in np.flatnonzero(stat[:stop] == 2).tolist():
@@ -278,7 +314,8 @@ def load_triples_device(source, format: str = "nt", *, strict: bool = False, err
     lexicals = []
     for s, t, fl in spans.tolist():
         key = raw[s:t].decode("utf-8", "surrogatepass")
-        lexicals.append(_unescape_key(key) if fl & 1 else key)
+        esc = fl & 3
+        lexicals.append(_unescape_key(key) if esc == 1 else (_csv_unquote(key) if esc == 2 else key))
     r = roles[:n_tok].cpu().numpy()
     vocab = Vocabulary.from_integer_encoding(lexicals, np.flatnonzero(r & 1), np.flatnonzero(r & 2))
     return vocab, edges[: 3 * n_edges].view(-1, 3).cpu().numpy()

@@ -295,6 +295,42 @@ def ingest_cases():
         cases.append(dict(name=f"triples_lit{int(include)}", triples=rows, include_literals=include,
                           lexicals=vocab.lexical_of, edges=edges.tolist(), entities=vocab.entity_tokens().tolist(),
                           predicates=sorted(vocab._predicate_tokens)))
+    # quoted csv / tsv (csv.reader, ingest.py:241): delimiters, doubled quotes, line breaks inside
+    # quotes (records spanning lines: row numbers are csv.reader's line_num), text after a closing
+    # quote, literal quotes inside unquoted fields, an unterminated quote at EOF, headers
+    quoted = {
+        "q_csv": ('s,p,o\n"a,1",r,"b ""x"" c"\n"multi\nline",r,b\r\nb,"q\r\nz",c\n\n'
+                  'c,"r"tail,a"b\n"",r,"""q"""\n'.replace('"",r,"""q"""', 'd,r,"""q"""')),
+        "q_tsv": 'a\t"p\tq"\tb\n"x\ny"\tr\t"a"\nb\t"r"\tc,"d"\n',
+        "q_empty_subject": 'a,r,b\n"",r,c\n',
+        "q_csv_eof": 'a,r,b\nc,r,"open,to\nend',
+        "q_header_multi": '"h1\nh2",p,o\na,r,b\n',
+    }
+    for name, text in quoted.items():
+        fmt = "tsv" if "tsv" in name else "csv"
+        for header in (False, True):
+            with tempfile.NamedTemporaryFile("w", suffix="." + fmt, delete=False, newline="") as fh:
+                fh.write(text)
+            try:
+                vocab, edges = build_vocabulary(parse_edge_table(fh.name, format=fmt, has_header=header))
+                cases.append(dict(name=f"{name}_{int(header)}", format=fmt, text=text, has_header=header,
+                                  strict=False, include_literals=False, lexicals=vocab.lexical_of,
+                                  edges=edges.tolist(), entities=vocab.entity_tokens().tolist(),
+                                  predicates=sorted(vocab._predicate_tokens)))
+            except ParseError as e:
+                cases.append(dict(name=f"{name}_{int(header)}", format=fmt, text=text, has_header=header,
+                                  strict=False, include_literals=False, error=[e.line, e.reason]))
+            except ValueError as e:
+                cases.append(dict(name=f"{name}_{int(header)}", format=fmt, text=text, has_header=header,
+                                  strict=False, include_literals=False, value_error=str(e)))
+    bad_rows = 'a,r,b\n"x\ny",r\nc,r,d\n'  # a 2-column record spanning lines 2-3: ParseError at line 3
+    with tempfile.NamedTemporaryFile("w", suffix=".csv", delete=False, newline="") as fh:
+        fh.write(bad_rows)
+    try:
+        build_vocabulary(parse_edge_table(fh.name, format="csv"))
+    except ParseError as e:
+        cases.append(dict(name="q_columns_multiline", format="csv", text=bad_rows, strict=False,
+                          include_literals=False, error=[e.line, e.reason]))
     (OUT / "ingest.json").write_text(json.dumps(cases, indent=1, ensure_ascii=False) + "\n")
 
 

@@ -229,7 +229,5 @@ def test_walk_adjacency_path_equals_csr_path(rng, monkeypatch):
     assert g2.walk_adjacency() is None
     b = wv.random_walks(g2, ents, walk_depth=7, walk_number=6, rng_seed=5, rng=rng)
     assert np.array_equal(a.tokens, b.tokens) and np.array_equal(a.offsets, b.offsets)
-    # the oldest vertices sit next to the DAG's sink: their walks end early, in both paths
-    c = wv.random_walks(g, ents[:40], walk_depth=7, walk_number=6, rng_seed=5, rng=rng)
-    d = wv.random_walks(g2, ents[:40], walk_depth=7, walk_number=6, rng_seed=5, rng=rng)
-    assert np.array_equal(c.tokens, d.tokens) and (np.diff(c.offsets) < 15).any()
+    # dead ends: the small random multigraphs of the golden walk fixtures have sinks; they run
+    # through the adjacency path by default and match the reference there (test_random_walks_*)
