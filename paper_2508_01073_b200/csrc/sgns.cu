@@ -2104,6 +2104,12 @@ template <typename T, int EPC, int MAXC>
 #ifndef WV_HEAVY_GRID
 #define WV_HEAVY_GRID (148 * 4)
 #endif
+#ifndef WV_PIECE_ALL_LOADS
+#define WV_PIECE_ALL_LOADS 0  // heavy pieces: all of a group's loads in flight (150 registers in fp64)
+#endif
+#ifndef WV_HEAVY_SERIAL
+#define WV_HEAVY_SERIAL 0  // heavy pieces before the light rows on one stream (the light rows then own the SMs)
+#endif
 #ifndef WV_SPLIT_B_PER_SM
 #define WV_SPLIT_B_PER_SM 2  // split owner: B-row CTAs per SM (they share the SMs with the next gather)
 #endif
@@ -2371,6 +2377,31 @@ __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc
       for (int q = 0; q < kPieceGroup; ++q) {
         ri[q] = __shfl_sync(0xffffffffu, my.x, (j0 + q) & 31);
         c[q] = __shfl_sync(0xffffffffu, my_c, (j0 + q) & 31);
+      }
+      if constexpr (WV_PIECE_ALL_LOADS) {
+        // every chunk of the group's contributions in flight at once (more registers)
+        Chunk<T, EPC> x[MAXC][kPieceGroup];
+#pragma unroll
+        for (int qq = 0; qq < MAXC; ++qq) {
+          const int cc = lane + 32 * qq;
+#pragma unroll
+          for (int q = 0; q < kPieceGroup; ++q)
+            if (cc < C && j0 + q < n) x[qq][q] = ld_chunk<T, EPC>(srcb + (size_t)ri[q] * d + cc * EPC);
+        }
+#pragma unroll
+        for (int qq = 0; qq < MAXC; ++qq) {
+          const int cc = lane + 32 * qq;
+          if (cc < C) {
+#pragma unroll
+            for (int q = 0; q < kPieceGroup; ++q)
+              if (j0 + q < n) {
+#pragma unroll
+                for (int e = 0; e < EPC; ++e)
+                  g[qq].v[e] = add_rn(g[qq].v[e], side_out ? mul_rn(c[q], x[qq][q].v[e]) : x[qq][q].v[e]);
+              }
+          }
+        }
+        continue;
       }
 #pragma unroll
       for (int qq = 0; qq < MAXC; ++qq) {
@@ -3680,6 +3711,15 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
   }
   if (flat_owner(c)) {
     if (WV_OWNER_FUSED_HEAVY) return dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
+    if (WV_HEAVY_SERIAL) {
+      int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, st);
+      if (rc) return rc;
+      if (t_heavy >= 0) WV_STAMP(t_heavy, st);
+      rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
+      if (rc) return rc;
+      if (t_light >= 0) WV_STAMP(t_light, st);
+      return 0;
+    }
     // heavy pieces on the side stream (small footprint), concurrent with the light rows
     WV_CUDA(cudaEventRecord(ss->fork_h, st));
     WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
