@@ -2,7 +2,9 @@
 (BA(1e7, m=10), 200 predicates, generated and encoded on the device), random walks
 depth 4 x 20 per entity (cfg5 walk parameters), one SGNS epoch at d=200 (window 5,
 5 negatives, the reference's 1 GiB batch rule), streamed over root blocks through
-SkipGramSession (parameters resident: 10M x 200 x 6 fp32 = 48 GB).
+SkipGramSession (parameters resident: 10M x 200 x 6 fp64 = 96 GB; fp32 halves it).
+
+    python profiles/northstar_e2e.py [n_entities] [roots_per_block] [fp64|fp32]
 
     python profiles/northstar_e2e.py [n_entities] [roots_per_block]
 
@@ -33,7 +35,8 @@ def main():
     torch.cuda.synchronize()
     t_graph = time.perf_counter() - t0
     cfg = wv.TrainConfig(vector_size=dim, window_size=5, negative_samples=5, learning_rate=0.01, epochs=1)
-    sess = wv.SkipGramSession(V, cfg, 42, precision="fp32")
+    prec = sys.argv[3] if len(sys.argv) > 3 else "fp64"  # the reference computes in float64
+    sess = wv.SkipGramSession(V, cfg, 42, precision=prec)
     n_roots = int(ents.numel())
     walk_s = sgns_s = 0.0
     hops = pairs = walks = 0
@@ -65,6 +68,7 @@ def main():
         "vocab": V, "walks": walks, "hops": hops, "pairs": pairs,
         "graph_build_s": t_graph, "walks_s": walk_s, "sgns_s": sgns_s, "walks_plus_sgns_s": total,
         "end_to_end_s": t_graph + total, "walk_hops_per_s": hops / walk_s, "sgns_pairs_per_s": pairs / sgns_s,
+        "precision": prec,
         "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
     }), flush=True)
 

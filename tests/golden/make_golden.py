@@ -432,27 +432,33 @@ def two_clique():
         rows += [(u, "p", v) for u in members for v in members if u != v]
     rows.append(("x0", "p", "y0"))
     vocab, edges, g = rows_graph(rows)
-    res = []
-    for seed in range(10):
-        corpus = random_walks(g, vocab.entity_tokens(), walk_depth=4, walk_number=25, rng_seed=42 + seed)
-        cfg = TrainConfig(min_count=1, vector_size=16, epochs=10, learning_rate=0.01, window_size=5,
-                          negative_samples=5)
-        model, losses = train(corpus, len(vocab), cfg, 42 + seed)
-        v = model.input_matrix
-        x = [vocab.token_of[f"x{i}"] for i in range(5)]
-        y = [vocab.token_of[f"y{i}"] for i in range(5)]
 
-        def cos(a, b):
-            return float(np.dot(v[a], v[b]) / (np.linalg.norm(v[a]) * np.linalg.norm(v[b])))
+    def band(dim):
+        res = []
+        for seed in range(10):
+            corpus = random_walks(g, vocab.entity_tokens(), walk_depth=4, walk_number=25, rng_seed=42 + seed)
+            cfg = TrainConfig(min_count=1, vector_size=dim, epochs=10, learning_rate=0.01, window_size=5,
+                              negative_samples=5)
+            model, losses = train(corpus, len(vocab), cfg, 42 + seed)
+            v = model.input_matrix
+            x = [vocab.token_of[f"x{i}"] for i in range(5)]
+            y = [vocab.token_of[f"y{i}"] for i in range(5)]
 
-        intra = [cos(a, b) for grp in (x, y) for a in grp for b in grp if a < b]
-        inter = [cos(a, b) for a in x for b in y]
-        res.append(dict(seed=42 + seed, margin=float(np.mean(intra) - np.mean(inter)), loss0=losses[0],
-                        loss_last=losses[-1]))
+            def cos(a, b):
+                return float(np.dot(v[a], v[b]) / (np.linalg.norm(v[a]) * np.linalg.norm(v[b])))
+
+            intra = [cos(a, b) for grp in (x, y) for a in grp for b in grp if a < b]
+            inter = [cos(a, b) for a in x for b in y]
+            res.append(dict(seed=42 + seed, margin=float(np.mean(intra) - np.mean(inter)), loss0=losses[0],
+                            loss_last=losses[-1]))
+        return res
+
+    # d 16 (the reference's own acceptance setting) and d 200 (the benchmark's width)
     (OUT / "two_clique.json").write_text(json.dumps(dict(edges=edges.tolist(), V=len(vocab),
                                                          x=[vocab.token_of[f"x{i}"] for i in range(5)],
                                                          y=[vocab.token_of[f"y{i}"] for i in range(5)],
-                                                         roots=vocab.entity_tokens().tolist(), runs=res), indent=1))
+                                                         roots=vocab.entity_tokens().tolist(), runs=band(16),
+                                                         runs_d200=band(200)), indent=1))
 
 
 def vocab_encoding():

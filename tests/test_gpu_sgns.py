@@ -237,3 +237,59 @@ def test_large_batch_replay_matches_oracle(wv):
     np.testing.assert_allclose(model.input_matrix, ref["inp"], rtol=0, atol=1e-10)
     np.testing.assert_allclose(model.output_matrix, ref["out"], rtol=0, atol=1e-10)
     np.testing.assert_allclose(losses, ref["losses"], rtol=1e-10)
+
+
+def _two_clique_margin(wv, ref, v):
+    def cos(a, b):
+        return float(np.dot(v[a], v[b]) / (np.linalg.norm(v[a]) * np.linalg.norm(v[b])))
+
+    x, y = ref["x"], ref["y"]
+    intra = [cos(a, b) for grp in (x, y) for a in grp for b in grp if a < b]
+    inter = [cos(a, b) for a in x for b in y]
+    return np.mean(intra) - np.mean(inter)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_two_clique_d200_device_streams_within_reference_band(wv, precision):
+    """The downstream check at the benchmark's width (d 200, reference band from 10 reference
+    runs in tests/golden/two_clique.json runs_d200): device streams, both stores."""
+    ref = json.loads((GOLDEN / "two_clique.json").read_text())
+    margins = np.array([r["margin"] for r in ref["runs_d200"]])
+    finals = np.array([r["loss_last"] for r in ref["runs_d200"]])
+    graph = wv.build_graph(np.array(ref["edges"]), ref["V"])
+    got_m, got_l = [], []
+    for r in ref["runs_d200"][:5]:
+        corpus = wv.random_walks(graph, ref["roots"], walk_depth=4, walk_number=25, rng_seed=r["seed"])
+        cfg = wv.TrainConfig(min_count=1, vector_size=200, epochs=10, learning_rate=0.01, window_size=5,
+                             negative_samples=5)
+        model, losses = wv.train(corpus, ref["V"], cfg, r["seed"], precision=precision)
+        got_m.append(_two_clique_margin(wv, ref, model.input_matrix))
+        got_l.append(losses[-1])
+    assert abs(np.mean(got_m) - margins.mean()) < 4 * margins.std() + 1e-3, (np.mean(got_m), margins.mean())
+    assert abs(np.mean(got_l) - finals.mean()) < 4 * finals.std() + 1e-3, (np.mean(got_l), finals.mean())
+
+
+def test_blockwise_session_within_reference_band(wv):
+    """SkipGramSession (the benchmark's trainer) streaming the corpus in root blocks -- a fresh
+    permutation per block, the session's resident parameters and RowAdam state -- against the
+    reference's downstream band at equal epochs (each epoch visits every block once; the batch
+    size is the reference's whole-corpus rule value)."""
+    ref = json.loads((GOLDEN / "two_clique.json").read_text())
+    margins = np.array([r["margin"] for r in ref["runs"]])
+    graph = wv.build_graph(np.array(ref["edges"]), ref["V"])
+    got = []
+    for r in ref["runs"][:5]:
+        roots = np.array(ref["roots"])
+        full = wv.random_walks(graph, roots, walk_depth=4, walk_number=25, rng_seed=r["seed"])
+        n_pairs = len(wv.generate_pairs(full, 5, 1, ref["V"])[0])
+        B = wv.suggest_batch_size(wv.estimate_per_sample_bytes("skipgram", 16, 5, 5), 1 << 30, n_pairs)
+        blocks = [wv.random_walks(graph, part, walk_depth=4, walk_number=25, rng_seed=r["seed"])
+                  for part in np.array_split(roots, 3)]
+        cfg = wv.TrainConfig(min_count=1, vector_size=16, epochs=1, learning_rate=0.01, window_size=5,
+                             negative_samples=5, batch_size=B)
+        sess = wv.SkipGramSession(ref["V"], cfg, r["seed"], precision="fp64")
+        for _ in range(10):
+            for blk in blocks:
+                sess.fit(blk, 1)
+        got.append(_two_clique_margin(wv, ref, sess.model.input_matrix))
+    assert abs(np.mean(got) - margins.mean()) < 4 * margins.std() + 1e-3, (np.mean(got), margins.mean())
