@@ -1784,6 +1784,9 @@ __global__ void __launch_bounds__(kOwnerBulkWarps * 32, 4) sgns_owner_bulk_kerne
 #ifndef WV_PIECE_GRID
 #define WV_PIECE_GRID 148
 #endif
+#ifndef WV_FLAT_SEGPF
+#define WV_FLAT_SEGPF 0  // load the next item's segment record one iteration ahead
+#endif
 #ifndef WV_FLAT_PREFETCH
 #define WV_FLAT_PREFETCH 0
 #endif
@@ -1922,6 +1925,26 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
     cp_async_wait<0>();
     return;
   }
+  // the next item's segment record is loaded one iteration ahead (its p/m/v addresses
+  // are then known at the top of the iteration: one dependent load less per item)
+  auto split_item = [&](uint32_t i, int32_t& c) -> uint32_t {
+    uint32_t r = __umulhi(i, A.cmag);
+    c = (int32_t)(i - r * C);
+    if (c < 0) {
+      --r;
+      c += (int32_t)C;
+    } else if (c >= (int32_t)C) {
+      ++r;
+      c -= (int32_t)C;
+    }
+    return r;
+  };
+  Segment sg_next;
+  int32_t c_next = 0;
+  if constexpr (WV_FLAT_SEGPF && kFlatU == 1) {
+    const uint32_t i_first = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i_first < total) sg_next = segs[split_item(i_first, c_next)];
+  }
   for (uint32_t i0 = blockIdx.x * blockDim.x * kFlatU + threadIdx.x; i0 < total; i0 += stride) {
     if (WV_FLAT_PREFETCH > 0) {
       // L2 prefetch of the optimizer-state rows this thread's item will touch
@@ -1955,20 +1978,22 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
     Segment sg[kFlatU];
     int32_t cr[kFlatU];
     bool ok[kFlatU];
+    if constexpr (WV_FLAT_SEGPF && kFlatU == 1) {
+      ok[0] = true;
+      sg[0] = sg_next;
+      cr[0] = c_next;
+      const uint32_t in_ = i0 + stride;
+      if (in_ < total) sg_next = segs[split_item(in_, c_next)];
+    } else {
 #pragma unroll
-    for (int u = 0; u < kFlatU; ++u) {
-      const uint32_t i = i0 + u * blockDim.x;
-      ok[u] = i < total;
-      uint32_t r = __umulhi(i, A.cmag);
-      cr[u] = (int32_t)(i - r * C);
-      if (cr[u] < 0) {
-        --r;
-        cr[u] += (int32_t)C;
-      } else if (cr[u] >= (int32_t)C) {
-        ++r;
-        cr[u] -= (int32_t)C;
+      for (int u = 0; u < kFlatU; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        ok[u] = i < total;
+        int32_t c;
+        const uint32_t r = split_item(i, c);
+        cr[u] = c;
+        if (ok[u]) sg[u] = segs[r];
       }
-      if (ok[u]) sg[u] = segs[r];
     }
     Chunk<T, EPC> p[kFlatU], m[kFlatU], vv[kFlatU], g[kFlatU];
 #pragma unroll

@@ -4,9 +4,8 @@ depth 4 x 20 per entity (cfg5 walk parameters), one SGNS epoch at d=200 (window 
 5 negatives, the reference's 1 GiB batch rule), streamed over root blocks through
 SkipGramSession (parameters resident: 10M x 200 x 6 fp64 = 96 GB; fp32 halves it).
 
-    python profiles/northstar_e2e.py [n_entities] [roots_per_block] [fp64|fp32]
+    python profiles/northstar_e2e.py [n_entities] [roots_per_block, 0 = all] [fp64|fp32]
 
-    python profiles/northstar_e2e.py [n_entities] [roots_per_block]
 
 Prints one JSON line: seconds for graph build, walks, SGNS, and the totals.
 """
@@ -24,7 +23,9 @@ def main():
     from paper_2508_01073_b200 import synth, walks as wmod
 
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
-    R = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
+    # roots per block; default (0) = all entities in one block: one global permutation over the
+    # whole corpus per epoch, exactly the reference's epoch (a 2e8-walk corpus fits in HBM)
+    R = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     depth, number, dim = 4, 20, 200
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -38,6 +39,7 @@ def main():
     prec = sys.argv[3] if len(sys.argv) > 3 else "fp64"  # the reference computes in float64
     sess = wv.SkipGramSession(V, cfg, 42, precision=prec)
     n_roots = int(ents.numel())
+    R = R or n_roots
     walk_s = sgns_s = 0.0
     hops = pairs = walks = 0
     torch.cuda.synchronize()

@@ -269,11 +269,14 @@ def test_two_clique_d200_device_streams_within_reference_band(wv, precision):
     assert abs(np.mean(got_l) - finals.mean()) < 4 * finals.std() + 1e-3, (np.mean(got_l), finals.mean())
 
 
-def test_blockwise_session_within_reference_band(wv):
+@pytest.mark.parametrize("blocks", ["strided", "whole"])
+def test_blockwise_session_within_reference_band(wv, blocks):
     """SkipGramSession (the benchmark's trainer) streaming the corpus in root blocks -- a fresh
     permutation per block, the session's resident parameters and RowAdam state -- against the
     reference's downstream band at equal epochs (each epoch visits every block once; the batch
-    size is the reference's whole-corpus rule value)."""
+    size is the reference's whole-corpus rule value).  Blocks must sample the roots (strided):
+    contiguous root ranges of a graph whose clusters follow the token order train one cluster at
+    a time and measured a margin of 0.29 against the band's 0.59 +- 0.04."""
     ref = json.loads((GOLDEN / "two_clique.json").read_text())
     margins = np.array([r["margin"] for r in ref["runs"]])
     graph = wv.build_graph(np.array(ref["edges"]), ref["V"])
@@ -283,13 +286,13 @@ def test_blockwise_session_within_reference_band(wv):
         full = wv.random_walks(graph, roots, walk_depth=4, walk_number=25, rng_seed=r["seed"])
         n_pairs = len(wv.generate_pairs(full, 5, 1, ref["V"])[0])
         B = wv.suggest_batch_size(wv.estimate_per_sample_bytes("skipgram", 16, 5, 5), 1 << 30, n_pairs)
-        blocks = [wv.random_walks(graph, part, walk_depth=4, walk_number=25, rng_seed=r["seed"])
-                  for part in np.array_split(roots, 3)]
+        parts = [roots[i::3] for i in range(3)] if blocks == "strided" else [roots]
+        blks = [wv.random_walks(graph, part, walk_depth=4, walk_number=25, rng_seed=r["seed"]) for part in parts]
         cfg = wv.TrainConfig(min_count=1, vector_size=16, epochs=1, learning_rate=0.01, window_size=5,
                              negative_samples=5, batch_size=B)
         sess = wv.SkipGramSession(ref["V"], cfg, r["seed"], precision="fp64")
         for _ in range(10):
-            for blk in blocks:
+            for blk in blks:
                 sess.fit(blk, 1)
         got.append(_two_clique_margin(wv, ref, sess.model.input_matrix))
     assert abs(np.mean(got) - margins.mean()) < 4 * margins.std() + 1e-3, (np.mean(got), margins.mean())
