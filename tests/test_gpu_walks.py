@@ -185,7 +185,8 @@ def test_cfg3_bfs_capped_on_cfg2_graph_bit_exact(wv):
 
     edges, V, ents, _ = synth.device_synthetic_kg("barabasi", 1_000_000, m=10, predicates=200, seed=7)
     graph = wv.build_graph(edges, V)
-    off, tgt, prd = graph.row_offsets, graph.col_targets, graph.col_predicates
+    # the oracle builds its own CSR from the edge list (graph.py:74-98 restated), not the device's
+    off, tgt, prd = ow.csr(edges.cpu().numpy(), V)
     ents = ents.cpu().numpy()
     roots = np.random.default_rng(5).choice(ents, 2000, replace=False)
     corpus, table = wv.bfs_walks(graph, roots, 4, max_walks_per_root=250)
