@@ -844,7 +844,7 @@ def run_ours(args, rank, world, local):
         off, tgt, prd = host_csr(g)
         cpu = cpu_baseline_leg(args, off, tgt, prd, ents.cpu().numpy(), V)
     fp32 = None
-    if args.precision == "fp64" and args.fp32_steps > 0:
+    if args.precision == "fp64" and args.fp32_steps > 0 and world == 1:
         fp32 = fp32_leg(args, wv, wmod, g, ents, V, block_range, torch, dev)
     configs = None
     if rank == 0 and world == 1 and args.configs not in ("", "none"):
