@@ -624,6 +624,9 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 #ifndef WV_GATHER_WARPS
 #define WV_GATHER_WARPS 8
 #endif
+#ifndef WV_GATHER_WARPS_WIDE
+#define WV_GATHER_WARPS_WIDE 5  // wide rows (fp64 d 200): 5 warps x 3 stages = 168 KB ring (4 warps: 88 -> 75 us with 5)
+#endif
 #ifndef WV_GATHER_PREFETCH
 #define WV_GATHER_PREFETCH 0  // pairs (per warp, in ring steps) whose rows are L2-prefetched ahead of their copies
 #endif
@@ -631,6 +634,7 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 #define WV_GATHER_STAGES 3  // 3 x 8 warps: one 134 KB CTA per SM leaves room for the side stream (+2.7 % vs 2 x 8)
 #endif
 constexpr int kBulkWarps = WV_GATHER_WARPS;
+constexpr int kBulkWarpsWide = WV_GATHER_WARPS_WIDE;
 constexpr int kBulkStages = WV_GATHER_STAGES;  // pairs in flight per warp
 
 // Phase 1b (default path): warp per pair with the 2+k rows fetched by
@@ -2986,10 +2990,10 @@ struct LaunchPair {
       return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps>(a, in, out, smem, st);
     }
     // wide rows (float64, large vector_size): half the warps per CTA keep the ring in shared memory
-    const size_t smem_h = bulk_smem_bytes(kBulkWarps / 2, a.d, 2 + a.k, sizeof(T));
+    const size_t smem_h = bulk_smem_bytes(kBulkWarpsWide, a.d, 2 + a.k, sizeof(T));
     if (rows16 && smem_h <= kBulkSmemMax && getenv("WV_SGNS_REG_GATHER") == nullptr) {
-      if (a.k == 5) return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps / 2, 5>(a, in, out, smem_h, st);
-      return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps / 2>(a, in, out, smem_h, st);
+      if (a.k == 5) return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide, 5>(a, in, out, smem_h, st);
+      return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide>(a, in, out, smem_h, st);
     }
     sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
     WV_LAUNCH_CHECK();
