@@ -3557,7 +3557,7 @@ static PairArgs pair_args(const BatchCtx& c, int h) {
   pa.U = c.bw.U[h];
   pa.G = c.bw.G[h];
   pa.coef = c.bw.coef[h];
-  pa.flag = c.bw.half[h].flag;
+  pa.flag = WV_SPLIT_OWNER ? c.bw.half[h].flag : nullptr;  // row flags only feed the split owner
   pa.cnt = c.bw.half[h].cnt;
   pa.uniq = c.bw.half[h].uniq;
   pa.gctr = c.bw.half[h].gctr;
@@ -3655,7 +3655,7 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
   oa.U = c.bw.U[h];
   oa.G = c.bw.G[h];
   oa.coef = c.bw.coef[h];
-  oa.flag = x.flag;
+  oa.flag = WV_SPLIT_OWNER ? x.flag : nullptr;
   oa.seg_base = nullptr;
   oa.bookkeep = 1;
   oa.in = model->input;
