@@ -30,6 +30,9 @@ namespace wv {
 constexpr int kPairThreads = 256;
 constexpr int kPairWarps = kPairThreads / 32;
 constexpr int kOwnerThreads = 256;
+#ifndef WV_FP64_RCP
+#define WV_FP64_RCP 0  // float64 RowAdam with reciprocal bias corrections (A/B only; off keeps numpy's divisions)
+#endif
 #ifndef WV_OWNER_GROUP
 #define WV_OWNER_GROUP 2
 #endif
@@ -1384,7 +1387,12 @@ struct OwnerArgs {
 template <typename T>
 struct AdamBC {
   double bc1, bc2;
+#if WV_FP64_RCP
+  double r1, r2;
+  __device__ __forceinline__ AdamBC(double a, double b) : bc1(a), bc2(b), r1(1.0 / a), r2(1.0 / b) {}
+#else
   __device__ __forceinline__ AdamBC(double a, double b) : bc1(a), bc2(b) {}
+#endif
 };
 template <>
 struct AdamBC<float> {
@@ -1415,7 +1423,12 @@ __device__ __forceinline__ T adam_elem(T& p, T& m, T& v, T g, const AdamBC<T>& b
   if constexpr (sizeof(T) == 8) {
     m = add_rn(mul_rn(b1, m), mul_rn(omb1, g));
     v = add_rn(mul_rn(b2, v), mul_rn(mul_rn(omb2, g), g));
+#if WV_FP64_RCP
+    // reciprocal bias corrections (within an ulp of numpy's divisions; fewer registers)
+    upd = div_rn(mul_rn(lr, mul_rn(m, (T)bc.r1)), add_rn(sqrt_rn(mul_rn(v, (T)bc.r2)), eps));
+#else
     upd = div_rn(mul_rn(lr, div_rn(m, (T)bc.bc1)), add_rn(sqrt_rn(div_rn(v, (T)bc.bc2)), eps));
+#endif
   } else {
     m = fmaf(b1, m, omb1 * g);
     v = fmaf(b2, v, (omb2 * g) * g);
