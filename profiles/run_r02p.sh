@@ -2,7 +2,7 @@
 cd $GRAFT_REPO_ROOT
 python -m pytest tests -q -m gpu > gpurun_out/r02p_gpu.log 2>&1; tail -4 gpurun_out/r02p_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02p_smoke.txt 2>&1; tail -2 gpurun_out/r02p_smoke.txt
-/usr/bin/time -v python bench.py --steps 5 --warmup 3 > gpurun_out/r02p_bench.json 2> gpurun_out/r02p_bench.err
+python bench.py --steps 5 --warmup 3 > gpurun_out/r02p_bench.json 2> gpurun_out/r02p_bench.err
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r02p_bench_ref.json 2> gpurun_out/r02p_bench_ref.err
 BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes 1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 --e2e-steps 1 > gpurun_out/r02p_bench_2rank_gloo.json 2> gpurun_out/r02p_bench_2rank_gloo.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_r02p.csv python bench.py --steps 1 --warmup 3 --roots 256 --e2e-steps 0 --no-cpu-baseline --configs none --fp32-steps 0 > gpurun_out/r02p_launch_bench.log 2>&1
