@@ -1353,6 +1353,7 @@ struct OwnerArgs {
   const Segment* heavy;
   const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
   const uint32_t* seg_base;   // split owner: the launch's segments start at segs + *seg_base (null: 0)
+  uint32_t piece;             // heavy-row piece size (contributions)
   int bookkeep;               // 1: this launch advances the batch counters (one launch per batch)
   uint8_t* flag;              // row-key membership flags of this batch, cleared per row (null: none)
   const void* U;
@@ -2330,8 +2331,12 @@ __global__ void __launch_bounds__(kHeavyThreads, WV_HEAVY_MINB) sgns_heavy_kerne
 constexpr int kPiece = WV_PIECE;
 static_assert(kPiece >= 1 && kPiece <= 32, "heavy pieces map one contribution per lane");
 
+#ifndef WV_PIECE_FP64
+#define WV_PIECE_FP64 32  // float64 piece size (16 measured -3 %)
+#endif
+constexpr int kPieceMin = WV_PIECE_FP64 < kPiece ? WV_PIECE_FP64 : kPiece;
 __host__ __device__ __forceinline__ int64_t max_pieces(int64_t items) {
-  return items / kPiece + items / (kLightMax + 1) + 2;
+  return items / kPieceMin + items / (kLightMax + 1) + 2;
 }
 
 __global__ void __launch_bounds__(kHeavyThreads) heavy_order(OwnerArgs A, uint32_t* gctr, uint2* pieces) {
@@ -2378,7 +2383,7 @@ __global__ void __launch_bounds__(kHeavyThreads) heavy_order(OwnerArgs A, uint32
     }
     for (uint32_t i = threadIdx.x; i < sg.len; i += kHeavyThreads)
       ents[sg.start + i] = slot_entry(sorted[i], side_out, A.B, A.k, A.sm);
-    const uint32_t np = (sg.len + kPiece - 1) / kPiece;
+    const uint32_t np = (sg.len + A.piece - 1) / A.piece;
     if (threadIdx.x == 0) {
       s_pbase = atomicAdd(gctr + GC_PIECES, np);
       heavy[h].pad = s_pbase;
@@ -2406,9 +2411,9 @@ __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc
     const uint2 pd = A.pieces[pc];
     const Segment sg = A.heavy[pd.x];
     const bool side_out = sg.key >= (uint32_t)A.V;
-    const uint32_t np = (sg.len + kPiece - 1) / kPiece;
-    const uint32_t q0 = pd.y * kPiece;
-    const int n = (int)min((uint32_t)kPiece, sg.len - q0);
+    const uint32_t np = (sg.len + A.piece - 1) / A.piece;
+    const uint32_t q0 = pd.y * A.piece;
+    const int n = (int)min(A.piece, sg.len - q0);
     uint2 my = make_uint2(0, 0);
     T my_c = 1;
     if (lane < n) {
@@ -3671,6 +3676,7 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
   oa.flag = WV_SPLIT_OWNER ? x.flag : nullptr;
   oa.seg_base = nullptr;
   oa.bookkeep = 1;
+  oa.piece = model->precision == WV_FP64 ? (uint32_t)WV_PIECE_FP64 : (uint32_t)kPiece;
   oa.in = model->input;
   oa.out = model->output;
   oa.m_in = model->m_in;
