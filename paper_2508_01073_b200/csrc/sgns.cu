@@ -33,6 +33,13 @@ constexpr int kOwnerThreads = 256;
 #ifndef WV_FP64_RCP
 #define WV_FP64_RCP 0  // float64 RowAdam with reciprocal bias corrections (A/B only; off keeps numpy's divisions)
 #endif
+#ifndef WV_SINGLES
+#define WV_SINGLES 2  // single-contribution rows through sgns_owner_single_kernel: 0 never, 1 always, 2 float64
+                      // (fp64 +1.1 %; fp32 -13 %: its heavy pieces no longer hide behind the light rows)
+#endif
+#ifndef WV_SINGLE_MINB
+#define WV_SINGLE_MINB 4  // 64 registers (5: 48 with a 32-byte stack, -5 %)
+#endif
 #ifndef WV_OWNER_GROUP
 #define WV_OWNER_GROUP 2
 #endif
@@ -363,7 +370,8 @@ struct PairArgs {
 // The list order inside a row is arbitrary; the owner kernels restore slot
 // order (warp ranking / CTA radix sort) before summing, so results are
 // deterministic, and reset cnt[key] to 0 for the next batch.
-enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3, GC_PIECES = 4, GC_NA = 5, GC_NB = 6 };
+enum { GC_UNIQUE = 0, GC_TOTAL = 1, GC_LIGHT = 2, GC_HEAVY = 3, GC_PIECES = 4, GC_NA = 5, GC_NB = 6,
+       GC_SINGLE = 7 };
 
 // global row key (row, or V + row) -> local key of this rank, false if another rank owns it
 __device__ __forceinline__ bool owned_key(uint32_t key, int64_t V, int nshard, int shard, int64_t Vl, uint32_t& lk) {
@@ -1077,7 +1085,8 @@ __global__ void fill_bc_table(double2* tab) {
 __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __restrict__ cnt, uint32_t* gctr,
                                int64_t V, int sparse, int32_t* __restrict__ steps_in, int32_t* __restrict__ steps_out,
                                Segment* __restrict__ segs, Segment* __restrict__ heavy, int64_t max_unique,
-                               WvSgnsDevState* state, int64_t B, const double2* __restrict__ bc_table) {
+                               WvSgnsDevState* state, int64_t B, const double2* __restrict__ bc_table,
+                               Segment* __restrict__ singles) {
   const int lane = threadIdx.x & 31;
   // the batch's pairs are decoded: advance the decode cursor for the next batch
   if (blockIdx.x == 0 && threadIdx.x == 0) state->lo += B;
@@ -1097,32 +1106,36 @@ __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __re
       if (lane >= o) incl += n;
     }
     const bool is_heavy = ok && len > (uint32_t)kLightMax;
-    const uint32_t ml = __ballot_sync(0xffffffffu, ok && !is_heavy);
+    const bool is_single = singles != nullptr && ok && len == 1u;  // the lean single-contribution owner
+    const uint32_t ml = __ballot_sync(0xffffffffu, ok && !is_heavy && !is_single);
     const uint32_t mh = __ballot_sync(0xffffffffu, is_heavy);
-    __shared__ uint32_t wsum[3][32];
-    __shared__ uint32_t bbase[3];
+    const uint32_t ms = __ballot_sync(0xffffffffu, is_single);
+    __shared__ uint32_t wsum[4][32];
+    __shared__ uint32_t bbase[4];
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     if (lane == 31) {
       wsum[0][warp] = incl;
       wsum[1][warp] = __popc(ml);
       wsum[2][warp] = __popc(mh);
+      wsum[3][warp] = __popc(ms);
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 4) {
       uint32_t run = 0;
       for (int w = 0; w < nwarps; ++w) {
         const uint32_t v = wsum[threadIdx.x][w];
         wsum[threadIdx.x][w] = run;
         run += v;
       }
-      bbase[threadIdx.x] = run ? atomicAdd(gctr + (threadIdx.x == 0 ? GC_TOTAL : threadIdx.x == 1 ? GC_LIGHT
-                                                                                                   : GC_HEAVY), run)
-                               : 0u;
+      const int ctr = threadIdx.x == 0 ? GC_TOTAL : threadIdx.x == 1 ? GC_LIGHT : threadIdx.x == 2 ? GC_HEAVY
+                                                                                                   : GC_SINGLE;
+      bbase[threadIdx.x] = run ? atomicAdd(gctr + ctr, run) : 0u;
     }
     __syncthreads();
     const uint32_t start = bbase[0] + wsum[0][warp] + incl - len;
     const uint32_t lb = bbase[1] + wsum[1][warp];
     const uint32_t hb = bbase[2] + wsum[2][warp];
+    const uint32_t sb = bbase[3] + wsum[3][warp];
     __syncthreads();  // wsum / bbase are rewritten by the next iteration
     if (ok) {
       cnt[key] = start;  // becomes the placement cursor
@@ -1150,6 +1163,8 @@ __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __re
       const uint32_t below = (1u << lane) - 1u;
       if (is_heavy)
         heavy[hb + __popc(mh & below)] = sg;
+      else if (is_single)
+        singles[sb + __popc(ms & below)] = sg;
       else
         segs[lb + __popc(ml & below)] = sg;
     }
@@ -1300,7 +1315,16 @@ __device__ __forceinline__ uint2 slot_entry(uint32_t v, bool side_out, int64_t B
 // contribution (G row, coefficient 1).
 __global__ void group_order(Segment* __restrict__ segs, const uint32_t* __restrict__ gctr,
                             const uint32_t* __restrict__ list, uint2* __restrict__ ents, int64_t V, int64_t B, int k,
-                            SlotMap sm) {
+                            SlotMap sm, Segment* __restrict__ singles) {
+  if (singles != nullptr) {  // single-contribution rows: their one entry rides in the record
+    const uint32_t ns = *(volatile const uint32_t*)(gctr + GC_SINGLE);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+      const Segment sg = singles[i];
+      const uint2 e = slot_entry(list[sg.start], sg.key >= (uint32_t)V, B, k, sm);
+      singles[i].start = e.x;
+      singles[i].pad = e.y;
+    }
+  }
   const uint32_t nl = *(volatile const uint32_t*)(gctr + GC_LIGHT);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
     const Segment sg = segs[i];
@@ -1351,6 +1375,7 @@ struct OwnerArgs {
   const uint32_t* gctr;  // grouping counters (GC_PIECES: piece count)
   const Segment* segs;
   const Segment* heavy;
+  const Segment* singles;  // single-contribution light rows (count gctr[GC_SINGLE])
   const uint32_t* seg_count;  // [0] light segments, [1] heavy segments
   const uint32_t* seg_base;   // split owner: the launch's segments start at segs + *seg_base (null: 0)
   uint32_t piece;             // heavy-row piece size (contributions)
@@ -1823,6 +1848,60 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
 template <typename T, int EPC, int MAXC>
 __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc);
+// Single-contribution light rows (92 % of a cfg2 batch's unique rows): the row's one
+// contribution rides in its record (start = source U/G row, pad = coefficient), so a
+// (row, 16-byte chunk) item is p, m, v, one contribution chunk and the RowAdam update,
+// with no entry list -- fewer registers than the general light-row kernel, more CTAs.
+// Same arithmetic as sgns_owner_flat_kernel (g = 0 + contribution, adam_elem).
+template <typename T, int EPC>
+__global__ void __launch_bounds__(256, WV_SINGLE_MINB) sgns_owner_single_kernel(OwnerArgs A) {
+  const int d = A.d;
+  const uint32_t C = (uint32_t)(d / EPC);
+  const uint32_t total = *(volatile const uint32_t*)(A.gctr + GC_SINGLE) * C;
+  const T* U = (const T*)A.U;
+  const T* G = (const T*)A.G;
+  const T* coef = (const T*)A.coef;
+  const T lr = (T)A.lr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t r = __umulhi(i, A.cmag);
+    int32_t c = (int32_t)(i - r * C);
+    if (c < 0) {
+      --r;
+      c += (int32_t)C;
+    } else if (c >= (int32_t)C) {
+      ++r;
+      c -= (int32_t)C;
+    }
+    const Segment sg = A.singles[r];
+    const bool side_out = sg.key >= (uint32_t)A.V;
+    const int64_t row = side_out ? (int64_t)sg.key - A.V : (int64_t)sg.key;
+    const int64_t o = row * d + (int64_t)c * EPC;
+    T* P = (T*)(side_out ? A.out : A.in);
+    T* M = (T*)(side_out ? A.m_out : A.m_in);
+    T* Vv = (T*)(side_out ? A.v_out : A.v_in);
+    Chunk<T, EPC> p = ld_chunk_p<T, EPC>(P + o);
+    Chunk<T, EPC> m = ld_chunk_mv<T, EPC>(M + o);
+    Chunk<T, EPC> vv = ld_chunk_mv<T, EPC>(Vv + o);
+    const Chunk<T, EPC> x = ld_chunk<T, EPC>((side_out ? U : G) + (int64_t)sg.start * d + (int64_t)c * EPC);
+    const T cf = side_out ? __ldg(coef + sg.pad) : T(1);
+    const AdamBC<T> bc(sg.bc1, sg.bc2);
+    bool changed = false;
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) {
+      const T g = add_rn(T(0), side_out ? mul_rn(cf, x.v[e]) : x.v[e]);
+      changed |= adam_elem<T>(p.v[e], m.v[e], vv.v[e], g, bc, lr) != T(0);
+    }
+    st_chunk_p<T, EPC>(P + o, p);
+    st_chunk_mv<T, EPC>(M + o, m);
+    st_chunk_mv<T, EPC>(Vv + o, vv);
+    if (changed) (side_out ? A.modified_out : A.modified_in)[row] = 1;
+    if (c == 0) {
+      (side_out ? A.touched_out : A.touched_in)[row] = 1;
+      A.cnt[sg.key] = 0;
+    }
+  }
+}
+
 template <typename T, int EPC, int MAXC>
 __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(OwnerArgs A) {
   const int d = A.d;
@@ -1831,7 +1910,8 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
   const Segment* segs = A.segs + (A.seg_base ? *A.seg_base : 0u);
   if (A.bookkeep && blockIdx.x == 0 && threadIdx.x == 0) {
     WvSgnsDevState* st = A.state;
-    atomicAdd((unsigned long long*)&st->rows_updated, (unsigned long long)(A.gctr[GC_LIGHT] + A.gctr[GC_HEAVY]));
+    atomicAdd((unsigned long long*)&st->rows_updated,
+              (unsigned long long)(A.gctr[GC_LIGHT] + A.gctr[GC_HEAVY] + A.gctr[GC_SINGLE]));
     st->batch += 1;
     st->step += 1;
   }
@@ -3088,6 +3168,7 @@ struct BatchHalf {
   uint32_t* rank;    // [items] claim rank of each item within its row
   uint8_t* flag;     // [2V] 1 for every row key this half's batch touches (set by decode, cleared by the owner)
   Segment* segs2;    // light segments regrouped: rows the next batch also touches first (split owner)
+  Segment* singles;  // single-contribution rows (the lean owner)
 };
 
 struct BatchWs {
@@ -3140,6 +3221,7 @@ static int64_t carve_batch_ws(char* base, int64_t V, int d, int k, int R, int64_
     x.rowdone = (uint32_t*)take((items / (kLightMax + 1) + 1) * 4);  // zeroed per batch with gctr
     x.rank = (uint32_t*)take(items * 4);
     x.segs2 = (Segment*)take(items * (int64_t)sizeof(Segment));
+    x.singles = (Segment*)take(items * (int64_t)sizeof(Segment));
   }
   return off + 1024;
 }
@@ -3591,6 +3673,12 @@ static PairArgs pair_args(const BatchCtx& c, int h) {
 
 // the flat per-element owner serves sparse RowAdam (default); the warp-per-row
 // kernels remain for dense mode, split mode and WV_SGNS_BULK_OWNER=1
+static bool flat_owner(const BatchCtx& c);
+// single-contribution light rows go to the lean owner kernel (flat owner, sparse RowAdam)
+static bool singles_mode(const BatchCtx& c) {
+  return (WV_SINGLES == 1 || (WV_SINGLES == 2 && c.model->precision == WV_FP64)) && flat_owner(c) &&
+         !WV_SPLIT_OWNER && getenv("WV_NO_SINGLES") == nullptr;
+}
 static bool flat_owner(const BatchCtx& c) {
   return c.model->sparse && c.bw.gsum == nullptr && getenv("WV_SGNS_BULK_OWNER") == nullptr;
 }
@@ -3676,6 +3764,7 @@ static OwnerArgs owner_args(const BatchCtx& c, int h) {
   oa.flag = WV_SPLIT_OWNER ? x.flag : nullptr;
   oa.seg_base = nullptr;
   oa.bookkeep = 1;
+  oa.singles = x.singles;
   oa.piece = model->precision == WV_FP64 ? (uint32_t)WV_PIECE_FP64 : (uint32_t)kPiece;
   oa.in = model->input;
   oa.out = model->output;
@@ -3705,13 +3794,14 @@ static int enqueue_group(const BatchCtx& c, int h, cudaStream_t st) {
   WV_CUDA(bc_table(&bct));
   group_segments<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.uniq, x.cnt, x.gctr, c.V, m->sparse, m->steps_in,
                                                                   m->steps_out, x.segs, x.heavy, c.items, m->state,
-                                                                  c.B, bct);
+                                                                  c.B, bct, singles_mode(c) ? x.singles : nullptr);
   WV_LAUNCH_CHECK();
   group_place_rank<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.idx, x.rank, c.B, c.k, c.R, c.cw, c.Vtok,
                                                                     x.cnt, x.list, c.nshard, c.shard, c.V);
   WV_LAUNCH_CHECK();
   if (flat_owner(c)) {
-    group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, c.sm);
+    group_order<<<grid_for(c.items, 256, 148 * 8), 256, 0, st>>>(x.segs, x.gctr, x.list, x.ents, c.V, c.B, c.k, c.sm,
+                                                                 singles_mode(c) ? x.singles : nullptr);
     WV_LAUNCH_CHECK();
     OwnerArgs oa = owner_args(c, h);
     const size_t smem = (size_t)heavy_bitmap_words(c.items) * 4;
@@ -3737,6 +3827,28 @@ static int enqueue_gather(const BatchCtx& c, int h, cudaStream_t st) {
   const unsigned pgrid = grid_for(c.B, kPairWarps, 148 * 32);
   return dispatch_rows<LaunchPair>(m->precision, c.d, pa, (const void*)m->input, (const void*)m->output, pgrid, st);
 }
+
+template <typename T, int EPC, int MAXC>
+struct LaunchSingles {
+  static int run(const OwnerArgs& a0, cudaStream_t st) {
+    OwnerArgs a = a0;
+    const uint32_t C = (uint32_t)(a.d / EPC);
+    a.cmag = C > 1 ? (uint32_t)(0xFFFFFFFFull / C + 1ull) : 0xFFFFFFFFu;
+    static int resident[16] = {0};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 16 && resident[dev] == 0) {
+      int nb = 0;
+      WV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sgns_owner_single_kernel<T, EPC>, 256, 0));
+      resident[dev] = nb > 0 ? nb : 1;
+    }
+    WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int per = dev >= 0 && dev < 16 ? resident[dev] : 4;
+    sgns_owner_single_kernel<T, EPC><<<(unsigned)(sms * per), 256, 0, st>>>(a);
+    WV_LAUNCH_CHECK();
+    return 0;
+  }
+};
 
 template <typename T, int EPC, int MAXC>
 struct LaunchPieces {
@@ -3767,6 +3879,24 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
   if (part == 1) {
     oa.segs = c.bw.half[h].segs2;
     oa.seg_count = c.bw.half[h].gctr + GC_NA;
+  }
+  if (flat_owner(c) && part == 0 && singles_mode(c)) {
+    // heavy pieces (side stream) beside the multi-contribution light rows, then the single-
+    // contribution rows alone with every SM (the lean kernel's CTAs fill them)
+    WV_CUDA(cudaEventRecord(ss->fork_h, st));
+    WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
+    int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, ss->h,
+                                         (unsigned)(model->precision == WV_FP64 ? WV_SERIAL_PIECE_GRID : WV_PIECE_GRID));
+    if (rc) return rc;
+    if (t_heavy >= 0) WV_STAMP(t_heavy, ss->h);
+    rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
+    if (rc) return rc;
+    WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
+    WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
+    rc = dispatch_rows<LaunchSingles>(model->precision, d, oa, st);
+    if (rc) return rc;
+    if (t_light >= 0) WV_STAMP(t_light, st);
+    return 0;
   }
   if (flat_owner(c)) {
     if (WV_OWNER_FUSED_HEAVY) return dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
