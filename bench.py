@@ -595,6 +595,24 @@ def cfg5_walks(args, wv, wmod, synth, torch, ref, peak):
                         "note": "SURVEY §8d walk bytes (24 B/hop + 8 B/walk) / summed walk-kernel time "
                                 "(CUDA events); CSR 8.8 GB: not L2-resident"},
            "note": "cfg5's SGNS state (6 x 1e8 x 200 values) needs the row-sharded mode over >= 4 GPUs"}
+    # the same kernel against its measured DRAM traffic (ncu --set full of one cfg5 launch, committed):
+    # random 8-byte reads cost 64-byte fetches, so the algorithmic 24 B/hop undercounts what moves
+    cap = sorted((ROOT / "profiles" / "r02").glob("prof_random_walk_kernel_cfg5_*.raw.csv.gz"))
+    if cap:
+        import csv
+        import gzip
+
+        rows = list(csv.reader(gzip.open(cap[-1], "rt")))
+        dd = dict(zip(rows[0], zip(rows[2], rows[1])))
+        unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        byt_ncu = sum(float(dd[m][0].replace(",", "")) * unit.get(dd[m][1], 1)
+                      for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        dur = float(dd["gpu__time_duration.sum"][0].replace(",", "")) * (
+            1e-9 if dd["gpu__time_duration.sum"][1] == "nsecond" else 1e-6 if dd["gpu__time_duration.sum"][1] ==
+            "usecond" else 1e-3)
+        res["roofline"]["ncu_dram_gbs"] = byt_ncu / dur / 1e9
+        res["roofline"]["frac_of_measured_traffic"] = byt_ncu / dur / 1e9 / peak
+        res["roofline"]["ncu_source"] = str(cap[-1].relative_to(ROOT))
     if ref is not None and not args.no_cpu_baseline:
         off = g.row_offsets
         tgt, prd = g.col_targets, g.col_predicates
