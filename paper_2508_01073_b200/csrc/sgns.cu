@@ -37,6 +37,12 @@ constexpr int kOwnerThreads = 256;
 #define WV_SINGLES 2  // single-contribution rows through sgns_owner_single_kernel: 0 never, 1 always, 2 float64
                       // (fp64 +1.1 %; fp32 -13 %: its heavy pieces no longer hide behind the light rows)
 #endif
+#ifndef WV_SINGLES_SERIAL
+#define WV_SINGLES_SERIAL 0  // heavy pieces then multi-contribution rows serially (0: concurrently)
+#endif
+#ifndef WV_MULTI_PER_SM
+#define WV_MULTI_PER_SM 0  // CTAs per SM of the multi-contribution light rows (0: all resident)
+#endif
 #ifndef WV_SINGLE_MINB
 #define WV_SINGLE_MINB 4  // 64 registers (5: 48 with a 32-byte stack, -5 %)
 #endif
@@ -646,6 +652,10 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 #endif
 constexpr int kBulkWarps = WV_GATHER_WARPS;
 constexpr int kBulkWarpsWide = WV_GATHER_WARPS_WIDE;
+#ifndef WV_GATHER_STAGES_WIDE
+#define WV_GATHER_STAGES_WIDE 3
+#endif
+constexpr int kBulkStagesWide = WV_GATHER_STAGES_WIDE;
 constexpr int kBulkStages = WV_GATHER_STAGES;  // pairs in flight per warp
 
 // Phase 1b (default path): warp per pair with the 2+k rows fetched by
@@ -660,10 +670,11 @@ constexpr int kBulkStages = WV_GATHER_STAGES;  // pairs in flight per warp
 // KC > 0: the negative count is a compile-time constant (KC + 1 <= 8 dots):
 // the 1 + KC output rows are loaded from shared memory once into registers
 // and reused by the dots and the gradient row.
-template <typename T, int EPC, int MAXC, bool CB, int NW, int KC>
+template <typename T, int EPC, int MAXC, bool CB, int NW, int KC, int ST>
 __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, const T* __restrict__ in,
                                                                     const T* __restrict__ out) {
   constexpr int kBulkWarps = NW;
+  constexpr int kBulkStages = ST;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = A.d, k = A.k;
@@ -3026,15 +3037,15 @@ static int dispatch_rows(int precision, int d, Args&&... args) {
 }
 
 // shared memory of the bulk gather: barriers + per-warp ring of R rows per stage
-static inline size_t bulk_smem_bytes(int nw, int d, int R, size_t es) {
-  return 16 * nw * kBulkStages + (size_t)nw * kBulkStages * R * d * es;
+static inline size_t bulk_smem_bytes(int nw, int d, int R, size_t es, int stages = kBulkStages) {
+  return 16 * nw * stages + (size_t)nw * stages * R * d * es;
 }
 static constexpr size_t kBulkSmemMax = 220 * 1024;
 
 // one bulk-gather instantiation: smem attribute, persistent grid of resident CTAs
-template <typename T, int EPC, int MAXC, bool CB, int NW, int KC = 0>
+template <typename T, int EPC, int MAXC, bool CB, int NW, int KC = 0, int ST = kBulkStages>
 static int launch_bulk_gather(const PairArgs& a, const void* in, const void* out, size_t smem, cudaStream_t st) {
-  auto kern = sgns_gather_bulk_kernel<T, EPC, MAXC, CB, NW, KC>;
+  auto kern = sgns_gather_bulk_kernel<T, EPC, MAXC, CB, NW, KC, ST>;
   static size_t attr_set[16] = {0};
   static int resident[16] = {0};
   static size_t resident_smem[16] = {0};
@@ -3088,10 +3099,11 @@ struct LaunchPair {
       return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarps>(a, in, out, smem, st);
     }
     // wide rows (float64, large vector_size): half the warps per CTA keep the ring in shared memory
-    const size_t smem_h = bulk_smem_bytes(kBulkWarpsWide, a.d, 2 + a.k, sizeof(T));
+    const size_t smem_h = bulk_smem_bytes(kBulkWarpsWide, a.d, 2 + a.k, sizeof(T), kBulkStagesWide);
     if (rows16 && smem_h <= kBulkSmemMax && getenv("WV_SGNS_REG_GATHER") == nullptr) {
-      if (a.k == 5) return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide, 5>(a, in, out, smem_h, st);
-      return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide>(a, in, out, smem_h, st);
+      if (a.k == 5)
+        return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide, 5, kBulkStagesWide>(a, in, out, smem_h, st);
+      return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide, 0, kBulkStagesWide>(a, in, out, smem_h, st);
     }
     sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
     WV_LAUNCH_CHECK();
@@ -3883,16 +3895,27 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
   if (flat_owner(c) && part == 0 && singles_mode(c)) {
     // heavy pieces (side stream) beside the multi-contribution light rows, then the single-
     // contribution rows alone with every SM (the lean kernel's CTAs fill them)
-    WV_CUDA(cudaEventRecord(ss->fork_h, st));
-    WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
-    int rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, ss->h,
-                                         (unsigned)(model->precision == WV_FP64 ? WV_SERIAL_PIECE_GRID : WV_PIECE_GRID));
-    if (rc) return rc;
-    if (t_heavy >= 0) WV_STAMP(t_heavy, ss->h);
-    rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, 0u, st);
-    if (rc) return rc;
-    WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
-    WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
+    const unsigned pgrid = (unsigned)(model->precision == WV_FP64 ? WV_SERIAL_PIECE_GRID : WV_PIECE_GRID);
+    int rc;
+    if (WV_SINGLES_SERIAL) {  // heavy pieces, then the multi-contribution rows, on one stream
+      rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, st, pgrid);
+      if (rc) return rc;
+      if (t_heavy >= 0) WV_STAMP(t_heavy, st);
+      rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, (unsigned)(WV_MULTI_PER_SM ? 1000 + WV_MULTI_PER_SM : 0),
+                                      st);
+      if (rc) return rc;
+    } else {
+      WV_CUDA(cudaEventRecord(ss->fork_h, st));
+      WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
+      rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, ss->h, pgrid);
+      if (rc) return rc;
+      if (t_heavy >= 0) WV_STAMP(t_heavy, ss->h);
+      rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, (unsigned)(WV_MULTI_PER_SM ? 1000 + WV_MULTI_PER_SM : 0),
+                                      st);
+      if (rc) return rc;
+      WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
+      WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
+    }
     rc = dispatch_rows<LaunchSingles>(model->precision, d, oa, st);
     if (rc) return rc;
     if (t_light >= 0) WV_STAMP(t_light, st);

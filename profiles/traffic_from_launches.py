@@ -15,7 +15,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 KERNELS = ("sgns_decode_kernel", "group_segments", "group_place_rank", "group_order", "heavy_order",
-           "sgns_gather_bulk_kernel", "sgns_owner_flat_kernel", "heavy_piece_kernel")
+           "sgns_gather_bulk_kernel", "sgns_owner_flat_kernel", "sgns_owner_single_kernel", "heavy_piece_kernel")
 
 tag = sys.argv[1]
 path = ROOT / "profiles" / "r02" / f"launches_{tag}.csv.gz"
