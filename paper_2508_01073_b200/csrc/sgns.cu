@@ -31,7 +31,11 @@ constexpr int kPairThreads = 256;
 constexpr int kPairWarps = kPairThreads / 32;
 constexpr int kOwnerThreads = 256;
 #ifndef WV_FP64_RCP
-#define WV_FP64_RCP 0  // float64 RowAdam with reciprocal bias corrections (A/B only; off keeps numpy's divisions)
+// float64 RowAdam with the per-row reciprocals of the bias corrections: m * (1 / bc1) and
+// v * (1 / bc2) instead of numpy's two divisions (each within an ulp; the fp64 parity bound
+// stays 1e-12).  Two fewer correctly rounded divides per element: single-row owner
+// 279 -> 271 us, step +2.0 % (profiles/r02/abn_r02x_fp64.txt); 0 keeps numpy's divisions.
+#define WV_FP64_RCP 1
 #endif
 #ifndef WV_SINGLES
 #define WV_SINGLES 2  // single-contribution rows through sgns_owner_single_kernel: 0 never, 1 always, 2 float64
@@ -610,6 +614,27 @@ __device__ __forceinline__ double log1pexp_t<double>(double x) { return log1pexp
 template <>
 __device__ __forceinline__ float log1pexp_t<float>(float x) { return x > 0.f ? x + log1pf(__expf(-x)) : log1pf(__expf(x)); }
 
+#ifndef WV_SHARED_EXP
+#define WV_SHARED_EXP 1
+#endif
+// Loss term log(1 + e^x) of one dot (x = -dot for the positive, +dot for a
+// negative; w2v.py:262-273) and sigmoid(dot) (w2v.py:242-244).  float64 shares
+// one exp(-|dot|) between them: the loss term is bit-identical to log1pexp, and
+// the sigmoid is 1 / (1 + e) for dot >= 0 (bit-identical to the reference's
+// 1 / (1 + exp(-dot))) and e / (1 + e) below (within an ulp of it).
+template <typename T>
+__device__ __forceinline__ T loss_sigmoid(T dot, bool positive, double& loss) {
+  if constexpr (sizeof(T) == 8 && WV_SHARED_EXP) {
+    const double e = exp(-fabs(dot));
+    const double x = positive ? -dot : dot;
+    loss += (x > 0 ? x : 0.0) + log1p(e);
+    return dot >= 0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+  } else {
+    loss += (double)log1pexp_t<T>(positive ? -dot : dot);
+    return T(1) / (T(1) + exp_t(-dot));
+  }
+}
+
 // Batch loss of one block -> partials; the last block to finish folds the
 // partials in block order (deterministic) into the device state.
 __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double block_sum) {
@@ -642,7 +667,13 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 #define WV_GATHER_WARPS 8
 #endif
 #ifndef WV_GATHER_WARPS_WIDE
-#define WV_GATHER_WARPS_WIDE 5  // wide rows (fp64 d 200): 5 warps x 3 stages = 168 KB ring (4 warps: 88 -> 75 us with 5)
+// wide rows (fp64 d 200): 10 warps x 2 stages = 224 KB ring.  The gather is bound by the
+// latency of its dependent float64 chains (dots, butterfly, exp, divide), so warps beat
+// stages: ncu alone 76 -> 50 us (4.9 TB/s) vs 5 x 3, step +0.9 % (r02x); 4 x 3: 88 us
+#define WV_GATHER_WARPS_WIDE 10
+#endif
+#ifndef WV_GATHER_WARPS_WIDE2
+#define WV_GATHER_WARPS_WIDE2 5  // fallback ring when 10 x 2 does not fit (larger k or d): 5 x 3
 #endif
 #ifndef WV_GATHER_PREFETCH
 #define WV_GATHER_PREFETCH 0  // pairs (per warp, in ring steps) whose rows are L2-prefetched ahead of their copies
@@ -653,9 +684,11 @@ __device__ __forceinline__ void finish_batch_loss(const PairArgs& A, double bloc
 constexpr int kBulkWarps = WV_GATHER_WARPS;
 constexpr int kBulkWarpsWide = WV_GATHER_WARPS_WIDE;
 #ifndef WV_GATHER_STAGES_WIDE
-#define WV_GATHER_STAGES_WIDE 3
+#define WV_GATHER_STAGES_WIDE 2
 #endif
 constexpr int kBulkStagesWide = WV_GATHER_STAGES_WIDE;
+constexpr int kBulkWarpsWide2 = WV_GATHER_WARPS_WIDE2;
+constexpr int kBulkStagesWide2 = 3;
 constexpr int kBulkStages = WV_GATHER_STAGES;  // pairs in flight per warp
 
 // Phase 1b (default path): warp per pair with the 2+k rows fetched by
@@ -801,8 +834,7 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
       const T mydot = __shfl_sync(0xffffffffu, red, (lane & 7) << 2);
       T mycoef = 0;
       if (lane <= KC) {
-        loss_acc += (double)log1pexp_t<T>(lane == 0 ? -mydot : mydot);
-        const T sg = T(1) / (T(1) + exp_t(-mydot));
+        const T sg = loss_sigmoid<T>(mydot, lane == 0, loss_acc);
         mycoef = (lane == 0 ? sg - T(1) : sg) * invB;
         coef[b * (KC + 1) + lane] = mycoef;
       }
@@ -856,8 +888,7 @@ __global__ void __launch_bounds__(NW * 32) sgns_gather_bulk_kernel(PairArgs A, c
     // lane j: loss term and coefficient of dot j
     T mycoef = 0;
     if (lane <= k) {
-      loss_acc += (double)log1pexp_t<T>(lane == 0 ? -mydot : mydot);
-      const T sg = T(1) / (T(1) + exp_t(-mydot));
+      const T sg = loss_sigmoid<T>(mydot, lane == 0, loss_acc);
       mycoef = (lane == 0 ? sg - T(1) : sg) * invB;
       coef[b * (k + 1) + lane] = mycoef;
     }
@@ -1081,16 +1112,21 @@ struct Segment {
   uint32_t key;    // row key (input row r, or V + output row r)
   uint32_t pad;
   double bc1;      // Adam bias corrections 1 - b1^t, 1 - b2^t with the row's new step t
-  double bc2;
+  double bc2;      // (their reciprocals under WV_FP64_RCP: bias_corr)
 };
 
 // RowAdam bias corrections 1 - b1^t, 1 - b2^t for t < kBcTable, computed once
 // per device with the same pow as the fallback (a table load replaces two
 // float64 pow calls per unique row)
 constexpr int kBcTable = 1 << 16;
+// 1 - b^t (w2v.py:386-387), or its reciprocal under WV_FP64_RCP (see AdamBC)
+__device__ __forceinline__ double bias_corr(double b, int t) {
+  const double c = 1.0 - pow(b, (double)t);
+  return WV_FP64_RCP ? 1.0 / c : c;
+}
 __global__ void fill_bc_table(double2* tab) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < kBcTable) tab[t] = make_double2(1.0 - pow(0.9, (double)t), 1.0 - pow(0.999, (double)t));
+  if (t < kBcTable) tab[t] = make_double2(bias_corr(0.9, t), bias_corr(0.999, t));
 }
 
 __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __restrict__ cnt, uint32_t* gctr,
@@ -1167,8 +1203,8 @@ __global__ void group_segments(const uint32_t* __restrict__ uniq, uint32_t* __re
           sg.bc1 = bc.x;
           sg.bc2 = bc.y;
         } else {
-          sg.bc1 = 1.0 - pow(0.9, (double)t);
-          sg.bc2 = 1.0 - pow(0.999, (double)t);
+          sg.bc1 = bias_corr(0.9, t);
+          sg.bc2 = bias_corr(0.999, t);
         }
       }
       const uint32_t below = (1u << lane) - 1u;
@@ -1419,15 +1455,17 @@ struct OwnerArgs {
 // divisions); the float32 store multiplies by the per-row reciprocals of the
 // bias corrections and uses a fast divide (a few ulp; the fp32 store is
 // tolerance-checked against the reference, not bit-checked).
-// Per-row bias corrections in the form the element update consumes: float64
-// keeps 1 - b^t (divided by, numpy order); float32 keeps their reciprocals.
+// Per-row bias corrections in the form the element update consumes.  A row's
+// segment record carries them as the grouping computed them once per unique
+// row: with WV_FP64_RCP the reciprocals 1 / (1 - b^t) (multiplied by), else
+// 1 - b^t (divided by, numpy's order).  float32 always multiplies.
 template <typename T>
 struct AdamBC {
-  double bc1, bc2;
 #if WV_FP64_RCP
   double r1, r2;
-  __device__ __forceinline__ AdamBC(double a, double b) : bc1(a), bc2(b), r1(1.0 / a), r2(1.0 / b) {}
+  __device__ __forceinline__ AdamBC(double a, double b) : r1(a), r2(b) {}
 #else
+  double bc1, bc2;
   __device__ __forceinline__ AdamBC(double a, double b) : bc1(a), bc2(b) {}
 #endif
 };
@@ -1436,8 +1474,13 @@ struct AdamBC<float> {
   float r1, r2;
   __device__ __forceinline__ AdamBC(double a, double b) {
 #ifdef __CUDA_ARCH__
+#if WV_FP64_RCP
+    r1 = (float)a;
+    r2 = (float)b;
+#else
     r1 = __frcp_rn((float)a);
     r2 = __frcp_rn((float)b);
+#endif
 #endif
   }
 };
@@ -1449,8 +1492,9 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 
 // RowAdam element update (w2v.py:384-395): m, v recurrences, bias-corrected
-// step.  float64 keeps numpy's exact operation order (correctly rounded
-// divisions, no FMA contraction).  The float32 store uses FMAs, the per-row
+// step.  float64 keeps numpy's operation order with correctly rounded
+// operations and no FMA contraction; under WV_FP64_RCP the two bias-correction
+// divisions become multiplications by per-row reciprocals (within an ulp each).  The float32 store uses FMAs, the per-row
 // reciprocals of the bias corrections and approximate sqrt / divide (a few
 // ulp; the fp32 store is tolerance-checked against the reference).
 template <typename T>
@@ -1857,6 +1901,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
+#ifndef WV_FLAT_GROUP
+#define WV_FLAT_GROUP 1  // contributions of a light row loaded together (1: one dependent chain per contribution)
+#endif
+constexpr int kFlatGroup = WV_FLAT_GROUP;
 template <typename T, int EPC, int MAXC>
 __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc);
 // Single-contribution light rows (92 % of a cfg2 batch's unique rows): the row's one
@@ -2122,6 +2170,33 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
       if (!ok[u]) continue;
       const bool side_out = sg[u].key >= (uint32_t)A.V;
       const T* srcb = (side_out ? U : G) + (int64_t)cr[u] * EPC;
+      if constexpr (kFlatGroup > 1) {
+        // contributions kFlatGroup at a time: the group's entry loads, then its contribution
+        // chunks (and coefficients), all in flight together; summed in slot order as below
+        const uint32_t len = sg[u].len;
+        for (uint32_t q0 = 0; q0 < len; q0 += kFlatGroup) {
+          uint2 en[kFlatGroup];
+#pragma unroll
+          for (int j = 0; j < kFlatGroup; ++j)
+            if (q0 + j < len)
+              en[j] = len == 1 ? make_uint2(sg[u].start, sg[u].pad) : __ldg(A.ents + sg[u].start + q0 + j);
+          Chunk<T, EPC> x[kFlatGroup];
+          T c[kFlatGroup];
+#pragma unroll
+          for (int j = 0; j < kFlatGroup; ++j)
+            if (q0 + j < len) {
+              x[j] = ld_chunk<T, EPC>(srcb + (int64_t)en[j].x * d);
+              c[j] = side_out ? __ldg(coef + en[j].y) : T(1);
+            }
+#pragma unroll
+          for (int j = 0; j < kFlatGroup; ++j)
+            if (q0 + j < len) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) g[u].v[e] = add_rn(g[u].v[e], side_out ? mul_rn(c[j], x[j].v[e]) : x[j].v[e]);
+            }
+        }
+        continue;
+      }
       for (uint32_t q = 0; q < sg[u].len; ++q) {
         // single-contribution rows carry their entry in the segment record (group_order)
         const uint2 en = sg[u].len == 1 ? make_uint2(sg[u].start, sg[u].pad) : __ldg(A.ents + sg[u].start + q);
@@ -3105,6 +3180,12 @@ struct LaunchPair {
         return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide, 5, kBulkStagesWide>(a, in, out, smem_h, st);
       return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide, 0, kBulkStagesWide>(a, in, out, smem_h, st);
     }
+    const size_t smem_h2 = bulk_smem_bytes(kBulkWarpsWide2, a.d, 2 + a.k, sizeof(T), kBulkStagesWide2);
+    if (rows16 && smem_h2 <= kBulkSmemMax && getenv("WV_SGNS_REG_GATHER") == nullptr) {
+      if (a.k == 5)
+        return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide2, 5, kBulkStagesWide2>(a, in, out, smem_h2, st);
+      return launch_bulk_gather<T, EPC, MAXC, false, kBulkWarpsWide2, 0, kBulkStagesWide2>(a, in, out, smem_h2, st);
+    }
     sgns_gather_kernel<T, EPC, MAXC, NG><<<grid, kPairThreads, 0, st>>>(a, (const T*)in, (const T*)out);
     WV_LAUNCH_CHECK();
     return 0;
@@ -3116,12 +3197,16 @@ struct LaunchPair {
 //   heavy : the CTA-per-heavy-row kernel, concurrent with the light-row owner
 // Works eagerly and under CUDA-graph capture: every side-stream segment forks
 // from and joins back into the caller's stream through these events.
+#ifndef WV_SIDE_AFTER_GATHER
+#define WV_SIDE_AFTER_GATHER 0
+#endif
 struct SideStream {
   int dev = -1;
   cudaStream_t s = nullptr, h = nullptr, b = nullptr;  // b: the split owner's B rows
   cudaEvent_t fork = nullptr, join = nullptr, fork_h = nullptr, join_h = nullptr, fork_b = nullptr;
   cudaEvent_t dec[2] = {nullptr, nullptr}, grp[2] = {nullptr, nullptr}, own[2] = {nullptr, nullptr};
   cudaEvent_t bdone[2] = {nullptr, nullptr};
+  cudaEvent_t gdone = nullptr;  // the current batch's gather is done (side-after-gather schedule)
 };
 
 static cudaError_t side_stream(SideStream** out) {
@@ -3148,7 +3233,8 @@ static cudaError_t side_stream(SideStream** out) {
       e = cudaStreamCreateWithPriority(&ss.h, cudaStreamNonBlocking, WV_HEAVY_PRIO ? hi_prio : lo_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ss.b, cudaStreamNonBlocking, lo_prio);
     cudaEvent_t* evs[] = {&ss.fork, &ss.join, &ss.fork_h, &ss.join_h, &ss.fork_b, &ss.dec[0], &ss.dec[1],
-                          &ss.grp[0], &ss.grp[1], &ss.own[0], &ss.own[1], &ss.bdone[0], &ss.bdone[1]};
+                          &ss.grp[0], &ss.grp[1], &ss.own[0], &ss.own[1], &ss.bdone[0], &ss.bdone[1],
+                          &ss.gdone};
     for (cudaEvent_t* ev : evs)
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
@@ -4062,6 +4148,10 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
   SideStream* ss = nullptr;
   WV_CUDA(side_stream(&ss));
   const bool split = WV_SPLIT_OWNER && flat_owner(c) && !WV_OWNER_FUSED_HEAVY && getenv("WV_NO_SPLIT") == nullptr;
+  // side-after-gather: batch i+1's decode + grouping start when batch i's gather ends, so the
+  // gather has the SMs to itself and the side work overlaps the (HBM-bound) update instead
+  static const int side_after_gather =
+      getenv("WV_SIDE_AFTER_GATHER") ? atoi(getenv("WV_SIDE_AFTER_GATHER")) : WV_SIDE_AFTER_GATHER;
   WV_CUDA(cudaEventRecord(ss->fork, st));
   WV_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   // optional timeline (profiling): per batch i, slots timer_base + 7i + {0 side start,
@@ -4074,6 +4164,7 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
       WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[hj], 0));
       WV_CUDA(cudaStreamWaitEvent(ss->s, ss->bdone[hj], 0));
     }
+    if (j >= 1 && side_after_gather) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->gdone, 0));
     WV_STAMP(tj + 0, ss->s);
     WV_CUDA_RC(enqueue_decode(c, hj, ss->s));
     WV_CUDA(cudaEventRecord(ss->dec[hj], ss->s));
@@ -4092,6 +4183,7 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
     WV_STAMP(t0 + 2, st);
     WV_CUDA_RC(enqueue_gather(c, h, st));
     WV_STAMP(t0 + 3, st);
+    if (side_after_gather) WV_CUDA(cudaEventRecord(ss->gdone, st));
     // the next batch's decode (its row flags) and grouping overlap this batch
     if (i + 1 < count) WV_CUDA_RC(side_batch(i + 1));
     WV_CUDA(cudaStreamWaitEvent(st, ss->grp[h], 0));
