@@ -820,6 +820,7 @@ def run_ours(args, rank, world, local):
     batch_bytes = pair_bytes + owner_bytes
     frac_8d = owner_bytes_8d / (kern["sgns_owner_adam(flat light rows + heavy pieces)"]["ms"] * 1e-3) / 1e9 / peak
     batch_ms = ph.get("batch", float("nan"))
+    batch_ms_timed = (ms / args.steps - walk_ms) / per
     # ncu DRAM traffic per launch of the owner phase's kernels (same batch geometry), newest capture
     traffic, traffic_src, batch_traffic = None, None, None
     tfs = sorted((ROOT / "profiles").glob("traffic_*.json"))
@@ -844,7 +845,13 @@ def run_ours(args, rank, world, local):
                        "unique_rows_per_batch": U,
                        "dram_traffic": batch_traffic,
                        "frac_of_measured_traffic": (batch_traffic / (batch_ms * 1e-3) / 1e9 / peak
-                                                    if batch_traffic else None)},
+                                                    if batch_traffic else None),
+                       # the batch period on the timed region's own clock (graph-replayed, no phase
+                       # events): (step time - walk kernel) / batches per step
+                       "timed": {"ms": batch_ms_timed, "gbs": batch_bytes / (batch_ms_timed * 1e-3) / 1e9,
+                                 "frac": batch_bytes / (batch_ms_timed * 1e-3) / 1e9 / peak,
+                                 "frac_of_measured_traffic": (batch_traffic / (batch_ms_timed * 1e-3) / 1e9 / peak
+                                                              if batch_traffic else None)}},
         # the same kernel against its measured DRAM bytes (the algorithmic figure counts a row
         # gathered by the pair phase and then updated by the Adam phase twice)
         "frac_of_measured_traffic": (traffic / (kern[dom]["ms"] * 1e-3) / 1e9 / peak if traffic else None),

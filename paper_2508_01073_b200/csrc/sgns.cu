@@ -44,6 +44,18 @@ constexpr int kOwnerThreads = 256;
 #ifndef WV_SINGLES_SERIAL
 #define WV_SINGLES_SERIAL 0  // heavy pieces then multi-contribution rows serially (0: concurrently)
 #endif
+#ifndef WV_SINGLES_CONCURRENT
+// 1: the single-contribution rows run beside the heavy pieces and multi-contribution rows
+// (which go to the high-priority stream ss->h) instead of after them; the singles kernel is
+// then launched as short-lived tiles (WV_SINGLE_TILE) so the latency-bound heavy / multi
+// CTAs take SM slots as soon as any free up and the singles fill the rest of the bandwidth
+// (fp64: +1.6 % over singles-after, tiles of 8 / 12 / 16 items per thread alike, 2: -8 %,
+// 32: -4 %; the heavy stream at low priority: -9 %; profiles/r02/abn_r02a[ab]_*.txt)
+#define WV_SINGLES_CONCURRENT 1
+#endif
+#ifndef WV_SINGLE_TILE
+#define WV_SINGLE_TILE 12  // (row, chunk) items per thread of one singles CTA in the concurrent schedule
+#endif
 #ifndef WV_MULTI_PER_SM
 #define WV_MULTI_PER_SM 0  // CTAs per SM of the multi-contribution light rows (0: all resident)
 #endif
@@ -1901,10 +1913,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 constexpr int kFlatU = WV_FLAT_U;  // (row, chunk) items per thread in flight
-#ifndef WV_FLAT_GROUP
-#define WV_FLAT_GROUP 1  // contributions of a light row loaded together (1: one dependent chain per contribution)
-#endif
-constexpr int kFlatGroup = WV_FLAT_GROUP;
+
 template <typename T, int EPC, int MAXC>
 __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc);
 // Single-contribution light rows (92 % of a cfg2 batch's unique rows): the row's one
@@ -1913,7 +1922,7 @@ __device__ __forceinline__ void heavy_piece_work(const OwnerArgs& A, uint32_t pc
 // with no entry list -- fewer registers than the general light-row kernel, more CTAs.
 // Same arithmetic as sgns_owner_flat_kernel (g = 0 + contribution, adam_elem).
 template <typename T, int EPC>
-__global__ void __launch_bounds__(256, WV_SINGLE_MINB) sgns_owner_single_kernel(OwnerArgs A) {
+__global__ void __launch_bounds__(256, WV_SINGLE_MINB) sgns_owner_single_kernel(OwnerArgs A, bool tiles) {
   const int d = A.d;
   const uint32_t C = (uint32_t)(d / EPC);
   const uint32_t total = *(volatile const uint32_t*)(A.gctr + GC_SINGLE) * C;
@@ -1921,7 +1930,7 @@ __global__ void __launch_bounds__(256, WV_SINGLE_MINB) sgns_owner_single_kernel(
   const T* G = (const T*)A.G;
   const T* coef = (const T*)A.coef;
   const T lr = (T)A.lr;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+  auto item = [&](uint32_t i) {
     uint32_t r = __umulhi(i, A.cmag);
     int32_t c = (int32_t)(i - r * C);
     if (c < 0) {
@@ -1958,6 +1967,17 @@ __global__ void __launch_bounds__(256, WV_SINGLE_MINB) sgns_owner_single_kernel(
       (side_out ? A.touched_out : A.touched_in)[row] = 1;
       A.cnt[sg.key] = 0;
     }
+  };
+  if (tiles) {  // one short-lived tile of blockDim.x * WV_SINGLE_TILE items (concurrent schedule)
+    const uint32_t base = blockIdx.x * blockDim.x * (uint32_t)WV_SINGLE_TILE + threadIdx.x;
+#pragma unroll 1
+    for (int j = 0; j < WV_SINGLE_TILE; ++j) {
+      const uint32_t i = base + (uint32_t)j * blockDim.x;
+      if (i >= total) break;
+      item(i);
+    }
+  } else {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) item(i);
   }
 }
 
@@ -2170,33 +2190,6 @@ __global__ void __launch_bounds__(256, WV_FLAT_MINB) sgns_owner_flat_kernel(Owne
       if (!ok[u]) continue;
       const bool side_out = sg[u].key >= (uint32_t)A.V;
       const T* srcb = (side_out ? U : G) + (int64_t)cr[u] * EPC;
-      if constexpr (kFlatGroup > 1) {
-        // contributions kFlatGroup at a time: the group's entry loads, then its contribution
-        // chunks (and coefficients), all in flight together; summed in slot order as below
-        const uint32_t len = sg[u].len;
-        for (uint32_t q0 = 0; q0 < len; q0 += kFlatGroup) {
-          uint2 en[kFlatGroup];
-#pragma unroll
-          for (int j = 0; j < kFlatGroup; ++j)
-            if (q0 + j < len)
-              en[j] = len == 1 ? make_uint2(sg[u].start, sg[u].pad) : __ldg(A.ents + sg[u].start + q0 + j);
-          Chunk<T, EPC> x[kFlatGroup];
-          T c[kFlatGroup];
-#pragma unroll
-          for (int j = 0; j < kFlatGroup; ++j)
-            if (q0 + j < len) {
-              x[j] = ld_chunk<T, EPC>(srcb + (int64_t)en[j].x * d);
-              c[j] = side_out ? __ldg(coef + en[j].y) : T(1);
-            }
-#pragma unroll
-          for (int j = 0; j < kFlatGroup; ++j)
-            if (q0 + j < len) {
-#pragma unroll
-              for (int e = 0; e < EPC; ++e) g[u].v[e] = add_rn(g[u].v[e], side_out ? mul_rn(c[j], x[j].v[e]) : x[j].v[e]);
-            }
-        }
-        continue;
-      }
       for (uint32_t q = 0; q < sg[u].len; ++q) {
         // single-contribution rows carry their entry in the segment record (group_order)
         const uint2 en = sg[u].len == 1 ? make_uint2(sg[u].start, sg[u].pad) : __ldg(A.ents + sg[u].start + q);
@@ -3225,7 +3218,7 @@ static cudaError_t side_stream(SideStream** out) {
 #define WV_SIDE_PRIO 1
 #endif
 #ifndef WV_HEAVY_PRIO
-#define WV_HEAVY_PRIO 0
+#define WV_HEAVY_PRIO WV_SINGLES_CONCURRENT
 #endif
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, WV_SIDE_PRIO ? hi_prio : lo_prio);
@@ -3928,7 +3921,7 @@ static int enqueue_gather(const BatchCtx& c, int h, cudaStream_t st) {
 
 template <typename T, int EPC, int MAXC>
 struct LaunchSingles {
-  static int run(const OwnerArgs& a0, cudaStream_t st) {
+  static int run(const OwnerArgs& a0, cudaStream_t st, bool tiles = false) {
     OwnerArgs a = a0;
     const uint32_t C = (uint32_t)(a.d / EPC);
     a.cmag = C > 1 ? (uint32_t)(0xFFFFFFFFull / C + 1ull) : 0xFFFFFFFFu;
@@ -3942,7 +3935,13 @@ struct LaunchSingles {
     }
     WV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int per = dev >= 0 && dev < 16 ? resident[dev] : 4;
-    sgns_owner_single_kernel<T, EPC><<<(unsigned)(sms * per), 256, 0, st>>>(a);
+    if (tiles) {
+      // grid for the largest possible singles count (every slot its own row); surplus tiles exit
+      const uint64_t items = (uint64_t)a.n_items * C, per_cta = 256ull * WV_SINGLE_TILE;
+      sgns_owner_single_kernel<T, EPC><<<(unsigned)((items + per_cta - 1) / per_cta), 256, 0, st>>>(a, true);
+    } else {
+      sgns_owner_single_kernel<T, EPC><<<(unsigned)(sms * per), 256, 0, st>>>(a, false);
+    }
     WV_LAUNCH_CHECK();
     return 0;
   }
@@ -3983,6 +3982,24 @@ static int enqueue_update(const BatchCtx& c, int h, SideStream* ss, cudaStream_t
     // contribution rows alone with every SM (the lean kernel's CTAs fill them)
     const unsigned pgrid = (unsigned)(model->precision == WV_FP64 ? WV_SERIAL_PIECE_GRID : WV_PIECE_GRID);
     int rc;
+    if (WV_SINGLES_CONCURRENT) {
+      // heavy pieces then the multi-contribution rows on the high-priority ss->h, beside the
+      // single-contribution rows' tiles on `st` (all three touch disjoint rows)
+      WV_CUDA(cudaEventRecord(ss->fork_h, st));
+      WV_CUDA(cudaStreamWaitEvent(ss->h, ss->fork_h, 0));
+      rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, ss->h, pgrid);
+      if (rc) return rc;
+      if (t_heavy >= 0) WV_STAMP(t_heavy, ss->h);
+      rc = dispatch_rows<LaunchOwner>(model->precision, d, oa, (unsigned)(WV_MULTI_PER_SM ? 1000 + WV_MULTI_PER_SM : 0),
+                                      ss->h);
+      if (rc) return rc;
+      rc = dispatch_rows<LaunchSingles>(model->precision, d, oa, st, true);
+      if (rc) return rc;
+      if (t_light >= 0) WV_STAMP(t_light, st);
+      WV_CUDA(cudaEventRecord(ss->join_h, ss->h));
+      WV_CUDA(cudaStreamWaitEvent(st, ss->join_h, 0));
+      return 0;
+    }
     if (WV_SINGLES_SERIAL) {  // heavy pieces, then the multi-contribution rows, on one stream
       rc = dispatch_rows<LaunchPieces>(model->precision, d, oa, st, pgrid);
       if (rc) return rc;
