@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
 from pathlib import Path
@@ -57,6 +58,7 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
     link += [str(objdir / (s + ".o")) for s in SOURCES]
     subprocess.run(link, check=True)
     os.replace(str(lib) + ".tmp", lib)
+    shutil.rmtree(objdir, ignore_errors=True)  # ~70 MB per variant; the repo snapshot travels to the GPU box
     return lib
 
 
