@@ -156,7 +156,7 @@ __device__ __forceinline__ void st_chunk(T* p, const Chunk<T, EPC>& c) {
 #define WV_OWNER_MV_STREAM 0  // loads and stores; measured slower (owner 151 -> 161 us)
 #endif
 #ifndef WV_OWNER_MV_STCS
-#define WV_OWNER_MV_STCS 0  // stores only
+#define WV_OWNER_MV_STCS 0  // stores only (fp64, with or without WV_OWNER_P_STCS: -1.2 %, r02ag)
 #endif
 #ifndef WV_OWNER_P_STCS
 #define WV_OWNER_P_STCS 0
@@ -176,6 +176,8 @@ template <typename T, int EPC>
 __device__ __forceinline__ void st_chunk_mv(T* p, const Chunk<T, EPC>& c) {
   if constexpr ((WV_OWNER_MV_STREAM || WV_OWNER_MV_STCS) && EPC * sizeof(T) == 16 && sizeof(T) == 4) {
     __stcs(reinterpret_cast<float4*>(p), make_float4(c.v[0], c.v[1], c.v[2], c.v[3]));
+  } else if constexpr (WV_OWNER_MV_STCS && EPC * sizeof(T) == 16 && sizeof(T) == 8) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(c.v[0], c.v[1]));
   } else {
     st_chunk<T, EPC>(p, c);
   }
@@ -210,6 +212,8 @@ template <typename T, int EPC>
 __device__ __forceinline__ void st_chunk_p(T* p, const Chunk<T, EPC>& c) {
   if constexpr (WV_OWNER_P_STCS && EPC * sizeof(T) == 16 && sizeof(T) == 4) {
     __stcs(reinterpret_cast<float4*>(p), make_float4(c.v[0], c.v[1], c.v[2], c.v[3]));
+  } else if constexpr (WV_OWNER_P_STCS && EPC * sizeof(T) == 16 && sizeof(T) == 8) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(c.v[0], c.v[1]));
   } else {
     st_chunk<T, EPC>(p, c);
   }
