@@ -829,7 +829,7 @@ def run_ours(args, rank, world, local):
         owner_parts = [k_ for k_ in t_ if k_.startswith("sgns_owner") or k_.startswith("heavy_piece")]
         if owner_parts:
             traffic = sum(t_[k_]["dram_bytes"] for k_ in owner_parts)
-            traffic_src = (f"{tfs[-1].relative_to(ROOT)}: ncu --set full dram__bytes_read+write of "
+            traffic_src = (f"{tfs[-1].relative_to(ROOT)}: ncu dram__bytes_read+write per launch of "
                            f"{' + '.join(sorted(owner_parts))}")
         batch_traffic = sum(v_["dram_bytes"] for k_, v_ in t_.items() if k_ != "random_walk_kernel")
         if "random_walk_kernel" in t_:  # CSR lookups: ncu DRAM bytes and L2 hit rate of the walk kernel

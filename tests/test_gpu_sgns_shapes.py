@@ -146,6 +146,25 @@ def test_cfg2_batches_replay(wv, cfg2, precision, atol):
     assert np.array_equal(model.output_matrix[~to], ref["out"][~to])
 
 
+@pytest.mark.parametrize("d,k", [(256, 5), (200, 7)])
+def test_fp64_fallback_ring_replay(wv, cfg1, d, k):
+    """float64 rows whose 10-warp x 2-stage gather ring does not fit shared memory
+    (R x d x 8 B x 20 > 220 KB: d 256 with k 5, or k 7 at d 200) take the 5 x 3 ring
+    (the compile-time k = 5 path and the runtime-k path); same 1e-12 bar."""
+    c = cfg1["corpus"]
+    n_w = 3000
+    tok, off = c.tokens[: c.offsets[n_w]], c.offsets[: n_w + 1]
+    B = 4096
+    ref = ov.train(tok, off, cfg1["V"], d, 5, k, 0.01, 0, 1, 42, batch=B)
+    cfg = wv.TrainConfig(vector_size=d, window_size=5, negative_samples=k, min_count=0, epochs=1,
+                         learning_rate=0.01, batch_size=B)
+    model, losses = wv.train(WalkCorpusHost(tok, off), cfg1["V"], cfg, 42, precision="fp64", pairs="numpy")
+    assert len(losses) == 1 and len(ref["pairs"]) > 8 * B
+    err = max(np.abs(model.input_matrix - ref["inp"]).max(), np.abs(model.output_matrix - ref["out"]).max())
+    assert err <= 1e-12, (d, k, err)
+    np.testing.assert_allclose(losses, ref["losses"], rtol=1e-12)
+
+
 # ------------------------------------------------- native decode / RNG --
 def _trainer(wv, corpus, V, cfg, seed=42):
     from paper_2508_01073_b200.w2v import _Trainer
