@@ -823,7 +823,8 @@ def run_ours(args, rank, world, local):
     batch_ms_timed = (ms / args.steps - walk_ms) / per
     # ncu DRAM traffic per launch of the owner phase's kernels (same batch geometry), newest capture
     traffic, traffic_src, batch_traffic = None, None, None
-    tfs = sorted((ROOT / "profiles").glob("traffic_*.json"))
+    # newest capture: tags grow in length through a round (r02y < r02ac < r02ai_full), then by name
+    tfs = sorted((ROOT / "profiles").glob("traffic_*.json"), key=lambda p_: (p_.stem[:11], len(p_.stem), p_.stem))
     if tfs:
         t_ = json.loads(tfs[-1].read_text())
         owner_parts = [k_ for k_ in t_ if k_.startswith("sgns_owner") or k_.startswith("heavy_piece")]

@@ -4185,10 +4185,11 @@ int wv_sgns_batches(const WvSgnsModel* model, const WvSgnsBatch* batch, void* ws
       WV_CUDA(cudaStreamWaitEvent(ss->s, ss->own[hj], 0));
       WV_CUDA(cudaStreamWaitEvent(ss->s, ss->bdone[hj], 0));
     }
-    if (j >= 1 && side_after_gather) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->gdone, 0));
+    if (j >= 1 && side_after_gather == 1) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->gdone, 0));
     WV_STAMP(tj + 0, ss->s);
     WV_CUDA_RC(enqueue_decode(c, hj, ss->s));
     WV_CUDA(cudaEventRecord(ss->dec[hj], ss->s));
+    if (j >= 1 && side_after_gather == 2) WV_CUDA(cudaStreamWaitEvent(ss->s, ss->gdone, 0));  // grouping only
     WV_CUDA_RC(enqueue_group(c, hj, ss->s));
     WV_STAMP(tj + 1, ss->s);
     WV_CUDA(cudaEventRecord(ss->grp[hj], ss->s));
