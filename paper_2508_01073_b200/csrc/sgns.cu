@@ -1112,7 +1112,10 @@ __global__ void __launch_bounds__(kPairThreads) sgns_gather_kernel(PairArgs A, c
 
 // Rows with more than kLightMax contributions in a batch (predicates, hub
 // entities) go to the CTA-per-row kernel; the rest to the warp-per-row one.
-constexpr int kLightMax = 16;
+#ifndef WV_LIGHT_MAX
+#define WV_LIGHT_MAX 16  // contributions of a light row; more go through the heavy pieces
+#endif
+constexpr int kLightMax = WV_LIGHT_MAX;
 constexpr int kHeavyThreads = 256;
 constexpr int kHeavyGroup = 8;            // rows loaded together per warp in the heavy kernel
 constexpr int64_t kBitmapMaxWords = 12288;  // slot bitmap in shared memory: batches up to 393,216 items
@@ -2495,7 +2498,7 @@ constexpr int kPiece = WV_PIECE;
 static_assert(kPiece >= 1 && kPiece <= 32, "heavy pieces map one contribution per lane");
 
 #ifndef WV_PIECE_FP64
-#define WV_PIECE_FP64 32  // float64 piece size (16 measured -3 %)
+#define WV_PIECE_FP64 64  // float64 piece size (concurrent schedule: 64 +0.9 %, 16 -1.2 % vs 32; r02ao)
 #endif
 constexpr int kPieceMin = WV_PIECE_FP64 < kPiece ? WV_PIECE_FP64 : kPiece;
 __host__ __device__ __forceinline__ int64_t max_pieces(int64_t items) {
