@@ -2500,7 +2500,8 @@ static_assert(kPiece >= 1 && kPiece <= 32, "heavy pieces map one contribution pe
 #ifndef WV_PIECE_FP64
 #define WV_PIECE_FP64 32  // float64 piece size (16 measured -3 %; at most 32: a piece's entries live one per lane)
 #endif
-static_assert(WV_PIECE_FP64 >= 1 && WV_PIECE_FP64 <= 32, "heavy pieces hold one entry per lane: at most 32 contributions");
+static_assert(WV_PIECE >= 1 && WV_PIECE <= 32 && WV_PIECE_FP64 >= 1 && WV_PIECE_FP64 <= 32,
+              "heavy pieces hold one entry per lane: at most 32 contributions");
 constexpr int kPieceMin = WV_PIECE_FP64 < kPiece ? WV_PIECE_FP64 : kPiece;
 __host__ __device__ __forceinline__ int64_t max_pieces(int64_t items) {
   return items / kPieceMin + items / (kLightMax + 1) + 2;
